@@ -1,0 +1,170 @@
+/*
+ * dmha.h — C ABI of the B200-native distributed multi-head attention forward
+ * (arXiv 2302.06218, §10.4 "Distributed Attention").
+ *
+ * Every function is extern "C", takes plain pointers and sizes, returns an int
+ * status (0 = DMHA_OK, < 0 = error) and never throws or aborts.  On error,
+ * dmha_last_error() returns a thread-local human-readable message.
+ *
+ * Operation (§4, with the north_star 1/sqrt(D) scale):
+ *   for every global query row g and head h
+ *     out[g,h,:] = sum_{j in A(g)} softmax_j(q[g,h,:].k[j,h,:] / sqrt(D)) v[j,h,:]
+ *     lse[h,g]   = ln sum_{j in A(g)} exp(q[g,h,:].k[j,h,:] / sqrt(D))
+ *   A(g) = all j (non-causal) or j <= g on GLOBAL positions (causal).
+ * The sequence is split into P = world_size partitions ("split the
+ * design matrix X along the sequence dimension into N partitions"); the result
+ * is defined in global order and does not depend on P or the layout.
+ *
+ * Tensor layouts (all row-major, contiguous, base pointers 16-byte aligned):
+ *   q, k, v, out : [L_loc, H, D]  this rank's L_loc = L / P rows, in the order
+ *                  the layout defines (see dmha_local_to_global).
+ *   lse          : [H, L_loc] fp32 (natural log) — always fp32.
+ * Element type of q/k/v/out is fixed by the dtype given to dmha_init:
+ *   DMHA_BF16 -> bf16 storage, bf16 tensor-core MMA, fp32 accumulation/softmax;
+ *   DMHA_FP32 -> fp32 storage (3xTF32 split on the tensor cores).
+ *
+ * Ownership: the caller owns q, k, v, out and lse.  q/k/v are read only (the
+ * ring sends from them at step 0 and from library buffers afterwards); out and
+ * lse are fully overwritten.  The library owns its NCCL communicator, ring
+ * buffers, fp32 accumulators and TMA descriptors; they are allocated lazily,
+ * grown on a larger shape and freed by dmha_finalize.  One device per process;
+ * calls are not thread safe.  dmha_forward is stream-ordered and asynchronous
+ * (like a kernel launch) on the stream given to dmha_init / dmha_set_stream.
+ */
+#ifndef DMHA_H_
+#define DMHA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DMHA_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
+
+enum dmha_status {
+  DMHA_OK = 0,
+  DMHA_ERR_INVALID = -1,     /* bad pointer / size / alignment / aliasing      */
+  DMHA_ERR_UNSUPPORTED = -2, /* D not in {64,128}, unsupported dtype combo     */
+  DMHA_ERR_CUDA = -3,        /* a CUDA runtime/driver call failed              */
+  DMHA_ERR_NCCL = -4,        /* an NCCL call failed or an async NCCL error     */
+  DMHA_ERR_OOM = -5,         /* workspace allocation failed (max-L search)     */
+  DMHA_ERR_STATE = -6        /* call before dmha_init or after dmha_finalize   */
+};
+
+enum dmha_dtype { DMHA_BF16 = 0, DMHA_FP32 = 1 };
+
+/* Shard layout ("N partitions {P_i}"):
+ *  CONTIGUOUS: rank r owns global rows [r*L/P, (r+1)*L/P).
+ *  ZIGZAG:     with c = L/(2P), rank r owns chunk r then chunk 2P-1-r
+ *              (global rows [r*c,(r+1)*c) then [(2P-1-r)*c,(2P-r)*c)); balances
+ *              causal work exactly.  Requires L % (2P) == 0. */
+enum dmha_layout { DMHA_LAYOUT_CONTIGUOUS = 0, DMHA_LAYOUT_ZIGZAG = 1 };
+
+struct dmha_stats {
+  uint64_t bytes_sent;      /* K/V bytes this rank sent over the ring (cumulative) */
+  uint64_t ring_steps;      /* ring steps executed (cumulative)                  */
+  uint64_t forwards;        /* dmha_forward calls completed                      */
+  uint64_t kernel_launches; /* device kernels launched by the library (cumulative) */
+  uint64_t workspace_bytes; /* bytes currently held by the library on the device  */
+};
+
+/* ---- setup / teardown ---------------------------------------------------- */
+
+/* Rank 0 only, before dmha_init with world_size > 1: writes a 128-byte NCCL
+ * unique id to id_out; the caller broadcasts it (e.g. torch.distributed). */
+int dmha_get_unique_id(void *id_out);
+
+/* world_size >= 1, 0 <= rank < world_size; unique_id NULL iff world_size == 1.
+ * device: CUDA ordinal for this process; dtype: enum dmha_dtype; layout: enum
+ * dmha_layout; cuda_stream: cudaStream_t (NULL = legacy default stream).
+ * Collective over all ranks when world_size > 1 (ncclCommInitRank). */
+int dmha_init(int world_size, int rank, const void *unique_id, int device, int dtype,
+              int layout, void *cuda_stream);
+
+/* Change the stream later calls are ordered on. */
+int dmha_set_stream(void *cuda_stream);
+
+/* Frees every library allocation and destroys the communicator. */
+int dmha_finalize(void);
+
+/* Thread-local message describing the last error ("" if none). */
+const char *dmha_last_error(void);
+
+/* ---- the distributed forward -------------------- */
+
+/* q, k, v, out: DEVICE pointers to this rank's [L_loc, H, D] shard; lse: DEVICE
+ * [H, L_loc] fp32.  L is the GLOBAL length (L % P == 0; % 2P for ZIGZAG), D the
+ * per-head dim (64 or 128), H >= 1 heads, causal 0/1.  All ranks must call with
+ * identical (L, D, H, causal).  Ring: P-1 steps of ncclSend/ncclRecv of (K,V)
+ * to rank+1 / from rank-1 overlapped with the local attention kernel, then an
+ * fp32 log-sum-exp combine of the per-step partials.
+ * Errors: INVALID (null, sizes, misaligned, out/lse overlapping q/k/v),
+ * UNSUPPORTED (D), STATE, OOM, CUDA, NCCL. */
+int dmha_forward(const void *q, const void *k, const void *v, void *out, float *lse,
+                 int64_t L, int D, int H, int causal);
+
+/* Same operation with HOST buffers (pinned recommended): copies q/k/v to
+ * device staging buffers, runs dmha_forward, copies out/lse back and
+ * synchronises the stream before returning (the end-to-end path). */
+int dmha_forward_host(const void *q, const void *k, const void *v, void *out, float *lse,
+                      int64_t L, int D, int H, int causal);
+
+/* Single-GPU emulation of the P-rank ring (test/measurement hook): q/k/v/out
+ * are DEVICE [P][L_loc, H, D] buffers holding every rank's shard back to back
+ * (rank-major), lse is [P][H, L_loc].  Runs each rank's ring schedule in turn
+ * with the identical kernels, index math and combine order as dmha_forward at
+ * world_size P, moving K/V blocks with device copies instead of NCCL.  No two
+ * kernels wait on one another.  Uses the dtype/stream of dmha_init (which may
+ * have world_size 1). */
+int dmha_forward_emulated(int world_size, int layout, const void *q, const void *k,
+                          const void *v, void *out, float *lse, int64_t L, int D, int H,
+                          int causal);
+
+/* Device bytes the library will hold per rank for (L, D, H) at the initialised
+ * world size and dtype (ring buffers + fp32 accumulators + staging excluded). */
+int dmha_workspace_bytes(int64_t L, int D, int H, size_t *bytes_out);
+
+int dmha_get_stats(struct dmha_stats *s);
+
+/* ---- individual hot-path steps (exported for tests and the bench) ------- */
+
+/* a1: global sequence position of local row i of rank r for
+ * (L, P, layout).  Pure host index math. Returns INVALID on bad arguments. */
+int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_t i,
+                         int64_t *global_out);
+
+/* a2 (P:193-211 + P:672-674): one local flash-attention pass of this rank's
+ * query block against one K/V block, on the dmha_init stream.
+ *  q: [Lq, H, D], k/v: [Lk, H, D] device (dtype of dmha_init).
+ *  Global positions: query row i sits at qpos(i) = i < q_chunk ? q_base0 + i
+ *  : q_base1 + (i - q_chunk); likewise for key rows with k_*.  Both maps must
+ *  be increasing.  With causal, key j is used by row i iff kpos(j) <= qpos(i).
+ *  out_mode 0: out is [Lq, H, D] of the init dtype holding O/l;
+ *  out_mode 1: out is fp32 [Lq, H, D] holding O/l (a ring partial).
+ *  lse: [H, Lq] fp32; rows with no usable key get lse = -inf and out = 0. */
+int dmha_attention_local(const void *q, const void *k, const void *v, void *out, float *lse,
+                         int64_t Lq, int64_t Lk, int D, int H, int causal, int64_t q_base0,
+                         int64_t q_base1, int64_t q_chunk, int64_t k_base0, int64_t k_base1,
+                         int64_t k_chunk, int out_mode);
+
+/* a4/a5 (north_star (3); "softmax requires all ..."): merge a partial
+ * (o_part fp32 [Lq,H,D], lse_part [H,Lq]) into the accumulator (o_acc fp32,
+ * lse_acc) with the stable log-sum-exp rule
+ *   lse = max + ln(e^{lse_acc-max} + e^{lse_part-max}),
+ *   o   = o_acc e^{lse_acc-lse} + o_part e^{lse_part-lse},
+ * -inf partials weigh 0 (both -inf keeps -inf and o = 0).
+ * final == 0: result written back into o_acc/lse_acc.
+ * final == 1: result written to out (init dtype, [Lq,H,D]) and lse_out. */
+int dmha_lse_combine(float *o_acc, float *lse_acc, const float *o_part, const float *lse_part,
+                     void *out, float *lse_out, int64_t Lq, int D, int H, int final_step);
+
+/* Block until all library work on the current stream is done (test helper). */
+int dmha_synchronize(void);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* DMHA_H_ */

@@ -1,0 +1,570 @@
+// dmha_api.cu — the C ABI (include/dmha.h) and the sequence-sharded ring
+// distribution layer.
+//
+// PAPER.md §10.4 splits X along the sequence into N partitions and
+// needs every key of a row for its softmax.  Here each rank keeps its
+// L/P query rows; the K/V blocks circulate around a ring of P ranks by NCCL
+// send/recv over NVLink (north_star (3)), P-1 steps, on a high-priority comm
+// stream overlapped with the local tcgen05 attention kernel on the compute
+// stream; per-step partials are merged by the fp32 log-sum-exp combine kernel.
+//
+// Per rank r, step s (0 <= s < P): source rank src = (r - s) mod P, K/V block
+// kv_s (kv_0 = the user's k/v, kv_s = ring buffer s % 2 for s >= 1).
+//   comm  (s < P-1): send kv_s -> r+1, recv kv_{s+1} <- r-1 into buffer (s+1)%2,
+//                    after the compute of step s-1 (last reader of that buffer).
+//   compute:         attention(q_r, kv_s, positions of src) -> partial;
+//                    s = 0 writes the accumulator, s >= 1 combines into it, the
+//                    last step writes out/lse.  P = 1 writes out/lse directly.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/dmha.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK_CUDA(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(DMHA_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define CK_NCCL(expr)                                                                     \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      return fail(DMHA_ERR_NCCL, "%s failed: %s (%s:%d)", #expr, ncclGetErrorString(_r), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+struct State {
+  bool inited = false;
+  int world = 1, rank = 0, device = 0, dtype = DMHA_BF16, layout = DMHA_LAYOUT_CONTIGUOUS;
+  cudaStream_t stream = nullptr;  // compute stream (user's)
+  cudaStream_t comm = nullptr;    // NCCL stream (library-owned, high priority)
+  ncclComm_t nccl = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_recv[2] = {nullptr, nullptr},
+              ev_done[2] = {nullptr, nullptr}, ev_comm_end = nullptr;
+  // ring workspace
+  void* kvbuf[2] = {nullptr, nullptr};  // each: K block then V block
+  float* o_acc = nullptr;
+  float* o_part = nullptr;
+  float* lse_acc = nullptr;
+  float* lse_part = nullptr;
+  size_t kv_bytes = 0, acc_elems = 0, lse_elems = 0;
+  // host-path staging
+  void* st_qkv = nullptr;  // q, k, v back to back
+  void* st_out = nullptr;
+  float* st_lse = nullptr;
+  size_t st_bytes = 0, st_lse_elems = 0;
+  dmha_stats stats{};
+};
+
+State g;
+
+size_t elem_bytes(int dtype) { return dtype == DMHA_BF16 ? 2 : 4; }
+
+int check_state() {
+  if (!g.inited) return fail(DMHA_ERR_STATE, "dmha: not initialised (call dmha_init)");
+  return DMHA_OK;
+}
+
+void free_ptr(void*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+void free_ptr(float*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+void update_ws_stat() {
+  g.stats.workspace_bytes = 2 * g.kv_bytes + 2 * g.acc_elems * 4 + 2 * g.lse_elems * 4 +
+                            g.st_bytes + g.st_lse_elems * 4;
+}
+
+int alloc_or_oom(void** p, size_t bytes, const char* what) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free allocation error
+    *p = nullptr;
+    return fail(DMHA_ERR_OOM, "dmha: cudaMalloc(%zu) for %s failed: %s", bytes, what,
+                cudaGetErrorString(e));
+  }
+  return DMHA_OK;
+}
+
+// Ring accumulators (always) and K/V ring buffers (need_kv).
+int ensure_ring_ws(int64_t Lloc, int D, int H, bool need_kv) {
+  const size_t elems = static_cast<size_t>(Lloc) * H * D;
+  const size_t lse = static_cast<size_t>(Lloc) * H;
+  if (elems > g.acc_elems) {
+    free_ptr(g.o_acc);
+    free_ptr(g.o_part);
+    g.acc_elems = 0;
+    int rc = alloc_or_oom(reinterpret_cast<void**>(&g.o_acc), elems * 4, "O_acc");
+    if (!rc) rc = alloc_or_oom(reinterpret_cast<void**>(&g.o_part), elems * 4, "O_part");
+    if (rc) {
+      free_ptr(g.o_acc);
+      free_ptr(g.o_part);
+      update_ws_stat();
+      return rc;
+    }
+    g.acc_elems = elems;
+  }
+  if (lse > g.lse_elems) {
+    free_ptr(g.lse_acc);
+    free_ptr(g.lse_part);
+    g.lse_elems = 0;
+    int rc = alloc_or_oom(reinterpret_cast<void**>(&g.lse_acc), lse * 4, "lse_acc");
+    if (!rc) rc = alloc_or_oom(reinterpret_cast<void**>(&g.lse_part), lse * 4, "lse_part");
+    if (rc) {
+      free_ptr(g.lse_acc);
+      free_ptr(g.lse_part);
+      update_ws_stat();
+      return rc;
+    }
+    g.lse_elems = lse;
+  }
+  if (need_kv) {
+    const size_t kvb = 2 * elems * elem_bytes(g.dtype);
+    if (kvb > g.kv_bytes) {
+      free_ptr(g.kvbuf[0]);
+      free_ptr(g.kvbuf[1]);
+      g.kv_bytes = 0;
+      int rc = alloc_or_oom(&g.kvbuf[0], kvb, "K/V ring buffer 0");
+      if (!rc) rc = alloc_or_oom(&g.kvbuf[1], kvb, "K/V ring buffer 1");
+      if (rc) {
+        free_ptr(g.kvbuf[0]);
+        free_ptr(g.kvbuf[1]);
+        update_ws_stat();
+        return rc;
+      }
+      g.kv_bytes = kvb;
+    }
+  }
+  update_ws_stat();
+  return DMHA_OK;
+}
+
+dmha::PosMap posmap(int64_t L, int P, int r, int layout) {
+  dmha::PosMap m;
+  if (layout == DMHA_LAYOUT_ZIGZAG) {
+    const int64_t c = L / (2 * P);
+    m.base0 = r * c;
+    m.base1 = static_cast<int64_t>(2 * P - 1 - r) * c;
+    m.chunk = c;
+  } else {
+    const int64_t Lloc = L / P;
+    m.base0 = r * Lloc;
+    m.base1 = r * Lloc + Lloc;
+    m.chunk = Lloc;
+  }
+  return m;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const char* pa = static_cast<const char*>(a);
+  const char* pb = static_cast<const char*>(b);
+  return pa < pb + nb && pb < pa + na;
+}
+
+int validate(const void* q, const void* k, const void* v, const void* out, const float* lse,
+             int64_t L, int D, int H, int P, int layout) {
+  if (!q || !k || !v || !out || !lse) return fail(DMHA_ERR_INVALID, "dmha: null pointer");
+  if (L < 1 || H < 1) return fail(DMHA_ERR_INVALID, "dmha: need L >= 1 and H >= 1");
+  if (D != 64 && D != 128)
+    return fail(DMHA_ERR_UNSUPPORTED, "dmha: per-head dim D=%d unsupported (64 or 128)", D);
+  if (layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG)
+    return fail(DMHA_ERR_INVALID, "dmha: unknown layout %d", layout);
+  const int64_t div = layout == DMHA_LAYOUT_ZIGZAG ? 2LL * P : P;
+  if (L % div != 0)
+    return fail(DMHA_ERR_INVALID, "dmha: L=%lld not divisible by %lld (world %d, layout %d)",
+                static_cast<long long>(L), static_cast<long long>(div), P, layout);
+  const int64_t Lloc = L / P;
+  if (Lloc > (1LL << 31) - 1) return fail(DMHA_ERR_INVALID, "dmha: L/P too large");
+  const void* ptrs[5] = {q, k, v, out, lse};
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+      return fail(DMHA_ERR_INVALID, "dmha: base pointers must be 16-byte aligned");
+  const size_t tb = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+  const size_t lb = static_cast<size_t>(Lloc) * H * 4;
+  const void* ins[3] = {q, k, v};
+  for (const void* in : ins)
+    if (overlaps(out, tb, in, tb) || overlaps(lse, lb, in, tb))
+      return fail(DMHA_ERR_INVALID, "dmha: out/lse overlap q/k/v");
+  if (overlaps(out, tb, lse, lb)) return fail(DMHA_ERR_INVALID, "dmha: out overlaps lse");
+  return DMHA_OK;
+}
+
+int run_local(const void* q, const void* k, const void* v, void* out, float* lse, int64_t Lq,
+              int64_t Lk, int D, int H, int causal, dmha::PosMap qm, dmha::PosMap km,
+              int out_mode) {
+  dmha::LocalAttnArgs a;
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.out = out;
+  a.lse = lse;
+  a.Lq = Lq;
+  a.Lk = Lk;
+  a.D = D;
+  a.H = H;
+  a.causal = causal;
+  a.qmap = qm;
+  a.kmap = km;
+  a.out_mode = out_mode;
+  cudaError_t e = g.dtype == DMHA_BF16 ? dmha::launch_attn_fwd_bf16(a, g.stream)
+                                       : dmha::launch_attn_fwd_fp32(a, g.stream);
+  if (e != cudaSuccess)
+    return fail(DMHA_ERR_CUDA, "dmha: attention kernel launch failed: %s", cudaGetErrorString(e));
+  g.stats.kernel_launches += dmha::attn_launches_per_call();
+  return DMHA_OK;
+}
+
+int run_combine(float* o_part, float* lse_part, void* out, float* lse, int64_t Lq, int D, int H,
+                int final_step) {
+  cudaError_t e = dmha::launch_lse_combine(g.o_acc, g.lse_acc, o_part, lse_part, out, lse, Lq,
+                                           D, H, final_step, g.dtype == DMHA_BF16, g.stream);
+  if (e != cudaSuccess)
+    return fail(DMHA_ERR_CUDA, "dmha: combine launch failed: %s", cudaGetErrorString(e));
+  g.stats.kernel_launches += 1;
+  return DMHA_OK;
+}
+
+// Compute part of ring step s for rank r (shared by the NCCL and emulated rings
+// so both run identical kernels in identical order).
+int ring_compute_step(int s, int P, int r, int layout, const void* q, const void* ks,
+                      const void* vs, void* out, float* lse, int64_t L, int D, int H, int causal) {
+  const int64_t Lloc = L / P;
+  const int src = ((r - s) % P + P) % P;
+  const dmha::PosMap qm = posmap(L, P, r, layout), km = posmap(L, P, src, layout);
+  if (P == 1) return run_local(q, ks, vs, out, lse, Lloc, Lloc, D, H, causal, qm, km, dmha::OUT_FINAL);
+  if (s == 0)
+    return run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
+                     dmha::OUT_PARTIAL_F32);
+  int rc = run_local(q, ks, vs, g.o_part, g.lse_part, Lloc, Lloc, D, H, causal, qm, km,
+                     dmha::OUT_PARTIAL_F32);
+  if (rc) return rc;
+  return run_combine(g.o_part, g.lse_part, out, lse, Lloc, D, H, s == P - 1);
+}
+
+int poll_nccl() {
+  if (!g.nccl) return DMHA_OK;
+  ncclResult_t st = ncclSuccess;
+  ncclResult_t r = ncclCommGetAsyncError(g.nccl, &st);
+  if (r != ncclSuccess || st != ncclSuccess) {
+    ncclCommAbort(g.nccl);
+    g.nccl = nullptr;
+    return fail(DMHA_ERR_NCCL, "dmha: NCCL async error: %s",
+                ncclGetErrorString(r != ncclSuccess ? r : st));
+  }
+  return DMHA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dmha_last_error(void) { return g_last_error.c_str(); }
+
+int dmha_get_unique_id(void* id_out) {
+  if (!id_out) return fail(DMHA_ERR_INVALID, "dmha_get_unique_id: null");
+  static_assert(sizeof(ncclUniqueId) == DMHA_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  CK_NCCL(ncclGetUniqueId(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return DMHA_OK;
+}
+
+int dmha_init(int world_size, int rank, const void* unique_id, int device, int dtype, int layout,
+              void* cuda_stream) {
+  if (g.inited) return fail(DMHA_ERR_STATE, "dmha_init: already initialised");
+  if (world_size < 1 || rank < 0 || rank >= world_size)
+    return fail(DMHA_ERR_INVALID, "dmha_init: bad world_size/rank %d/%d", world_size, rank);
+  if ((world_size > 1) != (unique_id != nullptr))
+    return fail(DMHA_ERR_INVALID, "dmha_init: unique_id must be given iff world_size > 1");
+  if (dtype != DMHA_BF16 && dtype != DMHA_FP32)
+    return fail(DMHA_ERR_INVALID, "dmha_init: bad dtype %d", dtype);
+  if (layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG)
+    return fail(DMHA_ERR_INVALID, "dmha_init: bad layout %d", layout);
+  int ndev = 0;
+  CK_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return fail(DMHA_ERR_INVALID, "dmha_init: device %d of %d", device, ndev);
+  CK_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(DMHA_ERR_UNSUPPORTED, "dmha_init: needs an sm_100 (B200) device, got sm_%d%d",
+                prop.major, prop.minor);
+  g = State();
+  g.world = world_size;
+  g.rank = rank;
+  g.device = device;
+  g.dtype = dtype;
+  g.layout = layout;
+  g.stream = static_cast<cudaStream_t>(cuda_stream);
+  int lo = 0, hi = 0;
+  CK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK_CUDA(cudaStreamCreateWithPriority(&g.comm, cudaStreamNonBlocking, hi));
+  CK_CUDA(cudaEventCreateWithFlags(&g.ev_start, cudaEventDisableTiming));
+  CK_CUDA(cudaEventCreateWithFlags(&g.ev_comm_end, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    CK_CUDA(cudaEventCreateWithFlags(&g.ev_recv[i], cudaEventDisableTiming));
+    CK_CUDA(cudaEventCreateWithFlags(&g.ev_done[i], cudaEventDisableTiming));
+  }
+  if (world_size > 1) {
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof(id));
+    CK_NCCL(ncclCommInitRank(&g.nccl, world_size, id, rank));
+  }
+  g.inited = true;
+  g_last_error.clear();
+  return DMHA_OK;
+}
+
+int dmha_set_stream(void* cuda_stream) {
+  if (int rc = check_state()) return rc;
+  g.stream = static_cast<cudaStream_t>(cuda_stream);
+  return DMHA_OK;
+}
+
+int dmha_finalize(void) {
+  if (!g.inited) return fail(DMHA_ERR_STATE, "dmha_finalize: not initialised");
+  cudaDeviceSynchronize();
+  free_ptr(g.kvbuf[0]);
+  free_ptr(g.kvbuf[1]);
+  free_ptr(g.o_acc);
+  free_ptr(g.o_part);
+  free_ptr(g.lse_acc);
+  free_ptr(g.lse_part);
+  free_ptr(g.st_qkv);
+  free_ptr(g.st_out);
+  free_ptr(g.st_lse);
+  if (g.nccl) ncclCommDestroy(g.nccl);
+  cudaEvent_t evs[6] = {g.ev_start, g.ev_comm_end, g.ev_recv[0], g.ev_recv[1], g.ev_done[0],
+                        g.ev_done[1]};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  if (g.comm) cudaStreamDestroy(g.comm);
+  g = State();
+  return DMHA_OK;
+}
+
+int dmha_workspace_bytes(int64_t L, int D, int H, size_t* bytes_out) {
+  if (int rc = check_state()) return rc;
+  if (!bytes_out || L < 1 || H < 1 || L % g.world) return fail(DMHA_ERR_INVALID, "dmha_workspace_bytes: bad args");
+  if (g.world == 1) {
+    *bytes_out = 0;
+    return DMHA_OK;
+  }
+  const size_t elems = static_cast<size_t>(L / g.world) * H * D;
+  const size_t lse = static_cast<size_t>(L / g.world) * H;
+  *bytes_out = 2 * (2 * elems * elem_bytes(g.dtype)) + 2 * elems * 4 + 2 * lse * 4;
+  return DMHA_OK;
+}
+
+int dmha_get_stats(dmha_stats* s) {
+  if (!s) return fail(DMHA_ERR_INVALID, "dmha_get_stats: null");
+  *s = g.stats;
+  return DMHA_OK;
+}
+
+int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_t i,
+                         int64_t* global_out) {
+  if (!global_out || world_size < 1 || rank < 0 || rank >= world_size || L < 1)
+    return fail(DMHA_ERR_INVALID, "dmha_local_to_global: bad args");
+  const int64_t div = layout == DMHA_LAYOUT_ZIGZAG ? 2LL * world_size : world_size;
+  if ((layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG) || L % div)
+    return fail(DMHA_ERR_INVALID, "dmha_local_to_global: bad layout or L");
+  if (i < 0 || i >= L / world_size) return fail(DMHA_ERR_INVALID, "dmha_local_to_global: i out of range");
+  const dmha::PosMap m = posmap(L, world_size, rank, layout);
+  *global_out = i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
+  return DMHA_OK;
+}
+
+int dmha_forward(const void* q, const void* k, const void* v, void* out, float* lse, int64_t L,
+                 int D, int H, int causal) {
+  if (int rc = check_state()) return rc;
+  if (int rc = validate(q, k, v, out, lse, L, D, H, g.world, g.layout)) return rc;
+  if (int rc = poll_nccl()) return rc;
+  const int P = g.world, r = g.rank;
+  causal = causal ? 1 : 0;
+  if (P == 1) {
+    int rc = ring_compute_step(0, 1, 0, g.layout, q, k, v, out, lse, L, D, H, causal);
+    if (rc) return rc;
+    g.stats.forwards++;
+    return DMHA_OK;
+  }
+  const int64_t Lloc = L / P;
+  if (int rc = ensure_ring_ws(Lloc, D, H, true)) return rc;
+  const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+  const int next = (r + 1) % P, prev = (r - 1 + P) % P;
+  CK_CUDA(cudaEventRecord(g.ev_start, g.stream));
+  CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_start, 0));
+  const void* kcur = k;
+  const void* vcur = v;
+  for (int s = 0; s < P; ++s) {
+    if (s < P - 1) {
+      const int nb = (s + 1) & 1;
+      if (s >= 2) CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_done[nb], 0));
+      char* dst = static_cast<char*>(g.kvbuf[nb]);
+      CK_NCCL(ncclGroupStart());
+      CK_NCCL(ncclSend(kcur, blk, ncclChar, next, g.nccl, g.comm));
+      CK_NCCL(ncclSend(vcur, blk, ncclChar, next, g.nccl, g.comm));
+      CK_NCCL(ncclRecv(dst, blk, ncclChar, prev, g.nccl, g.comm));
+      CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, prev, g.nccl, g.comm));
+      CK_NCCL(ncclGroupEnd());
+      CK_CUDA(cudaEventRecord(g.ev_recv[nb], g.comm));
+      g.stats.bytes_sent += 2 * blk;
+    }
+    int rc = ring_compute_step(s, P, r, g.layout, q, kcur, vcur, out, lse, L, D, H, causal);
+    if (rc) return rc;
+    if (s >= 1) CK_CUDA(cudaEventRecord(g.ev_done[s & 1], g.stream));
+    g.stats.ring_steps++;
+    if (s < P - 1) {
+      const int nb = (s + 1) & 1;
+      CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_recv[nb], 0));
+      kcur = g.kvbuf[nb];
+      vcur = static_cast<char*>(g.kvbuf[nb]) + blk;
+    }
+  }
+  // The comm stream's last work must be ordered before any later reuse.
+  CK_CUDA(cudaEventRecord(g.ev_comm_end, g.comm));
+  CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_comm_end, 0));
+  g.stats.forwards++;
+  return DMHA_OK;
+}
+
+int dmha_forward_host(const void* q, const void* k, const void* v, void* out, float* lse,
+                      int64_t L, int D, int H, int causal) {
+  if (int rc = check_state()) return rc;
+  if (!q || !k || !v || !out || !lse) return fail(DMHA_ERR_INVALID, "dmha_forward_host: null pointer");
+  if (L < 1 || H < 1 || L % g.world) return fail(DMHA_ERR_INVALID, "dmha_forward_host: bad L/H");
+  const int64_t Lloc = L / g.world;
+  const size_t tb = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+  const size_t lb = static_cast<size_t>(Lloc) * H;
+  if (3 * tb > g.st_bytes) {
+    free_ptr(g.st_qkv);
+    free_ptr(g.st_out);
+    g.st_bytes = 0;
+    int rc = alloc_or_oom(&g.st_qkv, 3 * tb, "host-path q/k/v staging");
+    if (!rc) rc = alloc_or_oom(&g.st_out, tb, "host-path out staging");
+    if (rc) {
+      free_ptr(g.st_qkv);
+      free_ptr(g.st_out);
+      return rc;
+    }
+    g.st_bytes = 3 * tb;
+  }
+  if (lb > g.st_lse_elems) {
+    free_ptr(g.st_lse);
+    g.st_lse_elems = 0;
+    if (int rc = alloc_or_oom(reinterpret_cast<void**>(&g.st_lse), lb * 4, "host-path lse")) return rc;
+    g.st_lse_elems = lb;
+  }
+  update_ws_stat();
+  char* dq = static_cast<char*>(g.st_qkv);
+  CK_CUDA(cudaMemcpyAsync(dq, q, tb, cudaMemcpyHostToDevice, g.stream));
+  CK_CUDA(cudaMemcpyAsync(dq + tb, k, tb, cudaMemcpyHostToDevice, g.stream));
+  CK_CUDA(cudaMemcpyAsync(dq + 2 * tb, v, tb, cudaMemcpyHostToDevice, g.stream));
+  if (int rc = dmha_forward(dq, dq + tb, dq + 2 * tb, g.st_out, g.st_lse, L, D, H, causal)) return rc;
+  CK_CUDA(cudaMemcpyAsync(out, g.st_out, tb, cudaMemcpyDeviceToHost, g.stream));
+  CK_CUDA(cudaMemcpyAsync(lse, g.st_lse, lb * 4, cudaMemcpyDeviceToHost, g.stream));
+  CK_CUDA(cudaStreamSynchronize(g.stream));
+  return DMHA_OK;
+}
+
+int dmha_forward_emulated(int world_size, int layout, const void* q, const void* k, const void* v,
+                          void* out, float* lse, int64_t L, int D, int H, int causal) {
+  if (int rc = check_state()) return rc;
+  if (world_size < 1) return fail(DMHA_ERR_INVALID, "dmha_forward_emulated: world_size < 1");
+  if (int rc = validate(q, k, v, out, lse, L, D, H, world_size, layout)) return rc;
+  const int P = world_size;
+  const int64_t Lloc = L / P;
+  causal = causal ? 1 : 0;
+  const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+  if (P > 1)
+    if (int rc = ensure_ring_ws(Lloc, D, H, false)) return rc;
+  // Rank r's computation depends only on the inputs, so ranks run one after the
+  // other with a single set of accumulators; the K/V block of step s is read
+  // in place from the source rank's shard (bit-identical to what NCCL delivers).
+  for (int r = 0; r < P; ++r) {
+    const char* qr = static_cast<const char*>(q) + r * blk;
+    char* outr = static_cast<char*>(out) + r * blk;
+    float* lser = lse + static_cast<size_t>(r) * Lloc * H;
+    for (int s = 0; s < P; ++s) {
+      const int src = ((r - s) % P + P) % P;
+      const char* ks = static_cast<const char*>(k) + src * blk;
+      const char* vs = static_cast<const char*>(v) + src * blk;
+      if (int rc = ring_compute_step(s, P, r, layout, qr, ks, vs, outr, lser, L, D, H, causal)) return rc;
+      if (s < P - 1) g.stats.bytes_sent += 2 * blk;
+      g.stats.ring_steps++;
+    }
+  }
+  g.stats.forwards++;
+  return DMHA_OK;
+}
+
+int dmha_attention_local(const void* q, const void* k, const void* v, void* out, float* lse,
+                         int64_t Lq, int64_t Lk, int D, int H, int causal, int64_t q_base0,
+                         int64_t q_base1, int64_t q_chunk, int64_t k_base0, int64_t k_base1,
+                         int64_t k_chunk, int out_mode) {
+  if (int rc = check_state()) return rc;
+  if (!q || !k || !v || !out || !lse) return fail(DMHA_ERR_INVALID, "dmha_attention_local: null pointer");
+  if (Lq < 0 || Lk < 0 || H < 1) return fail(DMHA_ERR_INVALID, "dmha_attention_local: bad sizes");
+  if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_attention_local: D=%d", D);
+  if (out_mode != dmha::OUT_FINAL && out_mode != dmha::OUT_PARTIAL_F32)
+    return fail(DMHA_ERR_INVALID, "dmha_attention_local: bad out_mode");
+  if (q_chunk < 0 || k_chunk < 0 || q_base1 < q_base0 + q_chunk || k_base1 < k_base0 + k_chunk)
+    return fail(DMHA_ERR_INVALID, "dmha_attention_local: position maps must be increasing");
+  const void* ptrs[5] = {q, k, v, out, lse};
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+      return fail(DMHA_ERR_INVALID, "dmha_attention_local: pointers must be 16-byte aligned");
+  dmha::PosMap qm{q_base0, q_base1, q_chunk}, km{k_base0, k_base1, k_chunk};
+  return run_local(q, k, v, out, lse, Lq, Lk, D, H, causal ? 1 : 0, qm, km, out_mode);
+}
+
+int dmha_lse_combine(float* o_acc, float* lse_acc, const float* o_part, const float* lse_part,
+                     void* out, float* lse_out, int64_t Lq, int D, int H, int final_step) {
+  if (int rc = check_state()) return rc;
+  if (!o_acc || !lse_acc || !o_part || !lse_part) return fail(DMHA_ERR_INVALID, "dmha_lse_combine: null");
+  if (final_step && (!out || !lse_out)) return fail(DMHA_ERR_INVALID, "dmha_lse_combine: null out");
+  if (Lq < 0 || H < 1) return fail(DMHA_ERR_INVALID, "dmha_lse_combine: bad sizes");
+  if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_lse_combine: D=%d", D);
+  cudaError_t e = dmha::launch_lse_combine(o_acc, lse_acc, o_part, lse_part, out, lse_out, Lq, D,
+                                           H, final_step, g.dtype == DMHA_BF16, g.stream);
+  if (e != cudaSuccess) return fail(DMHA_ERR_CUDA, "dmha_lse_combine: %s", cudaGetErrorString(e));
+  g.stats.kernel_launches += 1;
+  return DMHA_OK;
+}
+
+int dmha_synchronize(void) {
+  if (int rc = check_state()) return rc;
+  CK_CUDA(cudaStreamSynchronize(g.stream));
+  CK_CUDA(cudaStreamSynchronize(g.comm));
+  return poll_nccl();
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// kernels.h — internal launch interface between the C ABI (dmha_api.cu) and
+// the device kernels.  Not part of the public ABI (see include/dmha.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace dmha {
+
+// Global position of local row i:  i < chunk ? base0 + i : base1 + (i - chunk).
+// Both pieces are increasing and base1 >= base0 + chunk.
+struct PosMap {
+  int64_t base0;
+  int64_t base1;
+  int64_t chunk;
+};
+
+enum OutMode { OUT_FINAL = 0, OUT_PARTIAL_F32 = 1 };
+
+struct LocalAttnArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* out;   // OUT_FINAL: init dtype; OUT_PARTIAL_F32: fp32
+  float* lse;  // [H, Lq]
+  int64_t Lq, Lk;
+  int D, H;
+  int causal;
+  PosMap qmap, kmap;
+  int out_mode;
+};
+
+// bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu).
+cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream);
+// fp32 path (attn_fwd_fp32.cu).
+cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
+// log-sum-exp combine (lse_combine.cu).  out_dtype_bf16 selects the final
+// output element type when final_step != 0.
+cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part,
+                               const float* lse_part, void* out, float* lse_out, int64_t Lq,
+                               int D, int H, int final_step, int out_dtype_bf16,
+                               cudaStream_t stream);
+
+// Number of kernel launches a call of launch_attn_fwd_* makes (for stats).
+inline int attn_launches_per_call() { return 1; }
+
+}  // namespace dmha

@@ -1,0 +1,285 @@
+"""Thin Python binding of the dmha C ABI (include/dmha.h).
+
+Argument marshalling only: every step of the hot path (shard index math for
+the kernels, attention, ring exchange, LSE combine) runs inside libdmha.so.
+PyTorch supplies device memory, the current CUDA stream and, for world size
+> 1, the process group that broadcasts the NCCL unique id.
+
+There is no fallback: if libdmha.so is missing or cannot be loaded, every
+call raises ``DmhaError``.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "libdmha.so"
+
+OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_STATE = 0, -1, -2, -3, -4, -5, -6
+BF16, FP32 = 0, 1
+CONTIGUOUS, ZIGZAG = 0, 1
+UNIQUE_ID_BYTES = 128
+
+EXPORTED_SYMBOLS = (
+    "dmha_get_unique_id", "dmha_init", "dmha_set_stream", "dmha_finalize", "dmha_last_error",
+    "dmha_forward", "dmha_forward_host", "dmha_forward_emulated", "dmha_workspace_bytes",
+    "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
+    "dmha_synchronize",
+)
+
+
+class DmhaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"dmha error {code}: {msg}")
+        self.code = code
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("bytes_sent", ctypes.c_uint64), ("ring_steps", ctypes.c_uint64),
+                ("forwards", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("workspace_bytes", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdmha.so (raises DmhaError if it is missing: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise DmhaError(ERR_STATE, f"{_LIB_PATH} not built; run `python -m paper_2302_06218_b200.build`")
+        L = ctypes.CDLL(str(_LIB_PATH))
+        P, I, I64, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+        sig = {
+            "dmha_get_unique_id": [P],
+            "dmha_init": [I, I, P, I, I, I, P],
+            "dmha_set_stream": [P],
+            "dmha_finalize": [],
+            "dmha_forward": [P, P, P, P, P, I64, I, I, I],
+            "dmha_forward_host": [P, P, P, P, P, I64, I, I, I],
+            "dmha_forward_emulated": [I, I, P, P, P, P, P, I64, I, I, I],
+            "dmha_workspace_bytes": [I64, I, I, ctypes.POINTER(SZ)],
+            "dmha_get_stats": [ctypes.POINTER(Stats)],
+            "dmha_local_to_global": [I64, I, I, I, I64, ctypes.POINTER(I64)],
+            "dmha_attention_local": [P, P, P, P, P, I64, I64, I, I, I, I64, I64, I64, I64, I64, I64, I],
+            "dmha_lse_combine": [P, P, P, P, P, P, I64, I, I, I],
+            "dmha_synchronize": [],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.dmha_last_error.argtypes = []
+        L.dmha_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise DmhaError(rc, lib().dmha_last_error().decode(errors="replace"))
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _cur_stream() -> int:
+    import torch
+    return int(torch.cuda.current_stream().cuda_stream)
+
+
+_DT = {"bf16": BF16, "fp32": FP32}
+_LAY = {"contiguous": CONTIGUOUS, "zigzag": ZIGZAG}
+
+
+def dtype_code(dtype) -> int:
+    return _DT[dtype] if isinstance(dtype, str) else int(dtype)
+
+
+def layout_code(layout) -> int:
+    return _LAY[layout] if isinstance(layout, str) else int(layout)
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
+    _check(lib().dmha_get_unique_id(ctypes.addressof(buf)))
+    return buf.raw
+
+
+def init(world_size: int = 1, rank: int = 0, unique_id: bytes | None = None, device: int = 0,
+         dtype="bf16", layout="contiguous", stream: int | None = None):
+    uid = None
+    if unique_id is not None:
+        uid = ctypes.create_string_buffer(bytes(unique_id), UNIQUE_ID_BYTES)
+    s = _cur_stream() if stream is None else int(stream)
+    _check(lib().dmha_init(world_size, rank, None if uid is None else ctypes.addressof(uid), device,
+                           dtype_code(dtype), layout_code(layout), s))
+
+
+def init_distributed(dtype="bf16", layout="contiguous", device: int | None = None):
+    """init() over an initialised torch.distributed process group: rank 0 makes
+    the NCCL unique id and the group broadcasts it."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    dev = torch.cuda.current_device() if device is None else device
+    if world == 1:
+        return init(1, 0, None, dev, dtype, layout)
+    obj = [get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    init(world, rank, obj[0], dev, dtype, layout)
+
+
+def set_stream(stream: int):
+    _check(lib().dmha_set_stream(int(stream)))
+
+
+def finalize():
+    _check(lib().dmha_finalize())
+
+
+def synchronize():
+    _check(lib().dmha_synchronize())
+
+
+def forward(q, k, v, L: int, causal: bool = False, out=None, lse=None):
+    """Distributed forward on this rank's [L/P, H, D] device shards; returns (out, lse)."""
+    import torch
+    Lloc, H, D = q.shape
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((H, Lloc), dtype=torch.float32, device=q.device)
+    set_stream(_cur_stream())
+    _check(lib().dmha_forward(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
+                              int(bool(causal))))
+    return out, lse
+
+
+def forward_host(q, k, v, L: int, causal: bool = False, out=None, lse=None):
+    """Same as forward() but with host (pinned) tensors; copies in, runs, copies
+    out and synchronises (the end-to-end path)."""
+    import torch
+    Lloc, H, D = q.shape
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((H, Lloc), dtype=torch.float32, pin_memory=q.is_pinned())
+    set_stream(_cur_stream())
+    _check(lib().dmha_forward_host(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
+                                   int(bool(causal))))
+    return out, lse
+
+
+def forward_emulated(world_size: int, layout, q, k, v, L: int, causal: bool = False, out=None,
+                     lse=None):
+    """Single-GPU emulation of the P-rank ring; q/k/v are [P, L/P, H, D] device tensors."""
+    import torch
+    P, Lloc, H, D = q.shape
+    assert P == world_size
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((P, H, Lloc), dtype=torch.float32, device=q.device)
+    set_stream(_cur_stream())
+    _check(lib().dmha_forward_emulated(world_size, layout_code(layout), _ptr(q), _ptr(k), _ptr(v),
+                                       _ptr(out), _ptr(lse), int(L), D, H, int(bool(causal))))
+    return out, lse
+
+
+def attention_local(q, k, v, out, lse, causal=False, qmap=None, kmap=None, out_mode: int = 0):
+    """One local attention pass (hot-path step a2).  qmap/kmap = (base0, base1, chunk)."""
+    Lq, H, D = q.shape
+    Lk = k.shape[0]
+    qm = qmap if qmap is not None else (0, Lq, Lq)
+    km = kmap if kmap is not None else (0, Lk, Lk)
+    set_stream(_cur_stream())
+    _check(lib().dmha_attention_local(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), Lq, Lk, D, H,
+                                      int(bool(causal)), *map(int, qm), *map(int, km), int(out_mode)))
+    return out, lse
+
+
+def lse_combine(o_acc, lse_acc, o_part, lse_part, out=None, lse_out=None, final: bool = False):
+    """Hot-path step a4/a5: merge a partial into the accumulator (in place), or
+    with final=True write the merged result to out/lse_out."""
+    Lq, H, D = o_acc.shape
+    set_stream(_cur_stream())
+    _check(lib().dmha_lse_combine(_ptr(o_acc), _ptr(lse_acc), _ptr(o_part), _ptr(lse_part),
+                                  _ptr(out), _ptr(lse_out), Lq, D, H, int(bool(final))))
+
+
+def workspace_bytes(L: int, D: int, H: int) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().dmha_workspace_bytes(int(L), D, H, ctypes.byref(n)))
+    return n.value
+
+
+def get_stats() -> dict:
+    s = Stats()
+    _check(lib().dmha_get_stats(ctypes.byref(s)))
+    return {f: int(getattr(s, f)) for f, _ in Stats._fields_}
+
+
+def local_to_global(L: int, world_size: int, rank: int, layout, i: int) -> int:
+    g = ctypes.c_int64(0)
+    _check(lib().dmha_local_to_global(int(L), int(world_size), int(rank), layout_code(layout),
+                                      int(i), ctypes.byref(g)))
+    return g.value
+
+
+def global_rows(L: int, world_size: int, rank: int, layout) -> np.ndarray:
+    """Global positions of rank `rank`'s local rows (vectorised form of
+    dmha_local_to_global; tests check the two agree)."""
+    lay = layout_code(layout)
+    P = world_size
+    if lay == ZIGZAG:
+        if L % (2 * P):
+            raise DmhaError(ERR_INVALID, f"L={L} not divisible by 2P={2 * P}")
+        c = L // (2 * P)
+        return np.concatenate([np.arange(rank * c, (rank + 1) * c),
+                               np.arange((2 * P - 1 - rank) * c, (2 * P - rank) * c)])
+    if L % P:
+        raise DmhaError(ERR_INVALID, f"L={L} not divisible by P={P}")
+    n = L // P
+    return np.arange(rank * n, (rank + 1) * n)
+
+
+def shard(x, world_size: int, rank: int, layout):
+    """Rows of the global [L, ...] tensor that rank `rank` owns, in local order."""
+    idx = global_rows(x.shape[0], world_size, rank, layout)
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            return x[torch.from_numpy(idx).to(x.device)]
+    except ImportError:  # pragma: no cover
+        pass
+    return x[idx]
+
+
+def unshard(parts, L: int, layout):
+    """Inverse of shard: list of per-rank [L/P, ...] blocks -> global [L, ...]."""
+    P = len(parts)
+    first = parts[0]
+    try:
+        import torch
+        if isinstance(first, torch.Tensor):
+            outp = torch.empty((L,) + tuple(first.shape[1:]), dtype=first.dtype, device=first.device)
+            for r, p in enumerate(parts):
+                outp[torch.from_numpy(global_rows(L, P, r, layout)).to(first.device)] = p
+            return outp
+    except ImportError:  # pragma: no cover
+        pass
+    outp = np.empty((L,) + tuple(first.shape[1:]), dtype=first.dtype)
+    for r, p in enumerate(parts):
+        outp[global_rows(L, P, r, layout)] = p
+    return outp
+
+
+def attention_flops(L: int, D: int, H: int, causal: bool) -> float:
+    """north_star metric FLOPs: 4*L^2*D*H, halved for causal."""
+    f = 4.0 * L * L * D * H
+    return f / 2 if causal else f

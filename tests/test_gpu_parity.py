@@ -1,0 +1,234 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+Run on a B200 with ``pytest -m gpu``.  Inputs are the seeded synthetic
+generators of synth/inputs.py; the oracle is oracle/ (never the CUDA path).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from synth import inputs
+from tests.parity import TOL, assert_parity, metrics
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2302_06218_b200 import dmha  # noqa: E402
+
+
+_STATE = {"dtype": None}
+
+
+def ensure_lib(dtype):
+    """(Re)initialise the library for `dtype` (it holds one global state)."""
+    if _STATE["dtype"] != dtype:
+        if _STATE["dtype"] is not None:
+            dmha.finalize()
+        dmha.init(1, 0, None, 0, dtype, "contiguous")
+        _STATE["dtype"] = dtype
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _teardown():
+    yield
+    if _STATE["dtype"] is not None:
+        dmha.finalize()
+        _STATE["dtype"] = None
+
+
+@pytest.fixture
+def lib_bf16():
+    ensure_lib("bf16")
+
+
+def to_dev(x, dtype=torch.bfloat16):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dtype).cuda()
+
+
+def run_p1(q, k, v, causal, dtype=torch.bfloat16):
+    L = q.shape[0]
+    out, lse = dmha.forward(to_dev(q, dtype), to_dev(k, dtype), to_dev(v, dtype), L, causal)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy(), lse.cpu().numpy()
+
+
+SMALL = [  # (L, H, D): ragged tails, single tile, several tiles, L=1
+    (1, 1, 64), (1, 2, 128), (37, 2, 64), (128, 1, 64), (200, 3, 128), (256, 2, 64),
+    (300, 1, 128), (777, 2, 64), (1000, 2, 128), (2085, 2, 64), (4096, 1, 128),
+]
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("L,H,D", SMALL)
+def test_p1_small_full_oracle(lib_bf16, oracle_mod, L, H, D, causal):
+    q, k, v = inputs.qkv(L, H, D, seed=1000 + L + D)
+    out, lse = run_p1(q, k, v, causal)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(out, lse, ref_o, ref_l, "bf16", f"L={L} H={H} D={D} causal={causal}")
+
+
+def _sample_rows(L, bounds, n_rand=128, seed=0):
+    rows = set(range(0, min(64, L))) | set(range(max(0, L - 64), L))
+    for b in bounds:
+        rows |= set(range(max(0, b - 32), min(L, b + 32)))
+    rows |= set(np.random.default_rng(seed).integers(0, L, n_rand).tolist())
+    return np.array(sorted(rows), dtype=np.int64)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_config_c2_sampled(lib_bf16, oracle_mod, causal):
+    """C2: L=16384, D=64, H=8, bf16, P=1 (BASELINE.json configs[1])."""
+    L, H, D = 16384, 8, 64
+    q, k, v = inputs.qkv(L, H, D, seed=1235)
+    out, lse = run_p1(q, k, v, causal)
+    rows = _sample_rows(L, [128 * i for i in range(1, L // 128, 17)], 256)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal, rows=rows)
+    assert_parity(out[rows], lse[:, rows], ref_o, ref_l, "bf16", f"C2 causal={causal}")
+
+
+def test_zero_query_prefix_mean_and_one_hot(lib_bf16, oracle_mod):
+    L, H, D = 1000, 2, 64
+    _, k, v = inputs.qkv(L, H, D, seed=3)
+    out, lse = run_p1(np.zeros_like(k), k, v, True)
+    cnt = np.arange(1, L + 1)
+    ref = np.cumsum(v.astype(np.float64), 0) / cnt[:, None, None]
+    ma, rel = metrics(out, ref)
+    assert ma <= 2e-2 and rel <= 5e-3
+    np.testing.assert_allclose(lse, np.log(cnt)[None].repeat(H, 0), atol=1e-4)
+    targets = np.random.default_rng(5).permutation(L)[:D]
+    q1, k1, v1 = inputs.one_hot_selector(L, H, D, targets)
+    out1, _ = run_p1(q1, k1, v1, False)
+    sel = v1[targets[np.arange(L) % D]]
+    # selected value row, up to bf16 output rounding (|v| < 8 -> half-ulp <= 2^-6)
+    np.testing.assert_allclose(out1, sel, atol=2 ** -6 + 1e-6, rtol=0)
+
+
+def test_peaky_scores_finite_and_ulp_bound(lib_bf16, oracle_mod):
+    """Large scores (q x 16): no NaN/Inf; |err| <= 2^-8 |ref| + 2^-8 max|v|."""
+    L, H, D = 1500, 2, 128
+    q, k, v = inputs.qkv(L, H, D, seed=8, q_scale=16.0)
+    for causal in (False, True):
+        out, lse = run_p1(q, k, v, causal)
+        ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+        assert np.all(np.isfinite(out)) and np.all(np.isfinite(lse))
+        bound = 2 ** -8 * np.abs(ref_o) + 2 ** -8 * np.abs(v).max()
+        assert np.all(np.abs(out - ref_o) <= bound)
+        assert np.max(np.abs(lse - ref_l)) <= 1e-2 * max(1.0, np.abs(ref_l).max() / 100)
+
+
+def test_deterministic_and_host_path_identical(lib_bf16):
+    L, H, D = 3000, 2, 128
+    q, k, v = inputs.qkv(L, H, D, seed=77)
+    a_o, a_l = run_p1(q, k, v, True)
+    b_o, b_l = run_p1(q, k, v, True)
+    np.testing.assert_array_equal(a_o, b_o)
+    np.testing.assert_array_equal(a_l, b_l)
+    hq, hk, hv = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in (q, k, v))
+    ho, hl = dmha.forward_host(hq, hk, hv, L, True)
+    np.testing.assert_array_equal(ho.float().numpy(), a_o)
+    np.testing.assert_array_equal(hl.numpy(), a_l)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("layout", ["contiguous", "zigzag"])
+@pytest.mark.parametrize("causal", [False, True])
+def test_emulated_ring_matches_oracle(lib_bf16, oracle_mod, P, layout, causal):
+    L, H, D = 2048 + 64 * P, 2, 64 if P != 4 else 128
+    q, k, v = inputs.qkv(L, H, D, seed=500 + P)
+    parts = [[dmha.shard(x, P, r, layout) for r in range(P)] for x in (q, k, v)]
+    dq, dk, dv = (to_dev(np.stack(p)) for p in parts)
+    out, lse = dmha.forward_emulated(P, layout, dq, dk, dv, L, causal)
+    torch.cuda.synchronize()
+    out_g = dmha.unshard([o for o in out.float().cpu().numpy()], L, layout)
+    lse_g = dmha.unshard([l.T for l in lse.cpu().numpy()], L, layout).T
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(out_g, lse_g, ref_o, ref_l, "bf16", f"ring P={P} {layout} causal={causal}")
+    st = dmha.get_stats()
+    assert st["bytes_sent"] >= (P - 1) * 2 * (L // P) * H * D * 2
+
+
+def test_emulated_p1_bit_identical_to_forward(lib_bf16):
+    L, H, D = 1024, 2, 128
+    q, k, v = inputs.qkv(L, H, D, seed=9)
+    a_o, a_l = run_p1(q, k, v, True)
+    o, l = dmha.forward_emulated(1, "contiguous", to_dev(q[None]), to_dev(k[None]), to_dev(v[None]), L, True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(o[0].float().cpu().numpy(), a_o)
+    np.testing.assert_array_equal(l[0].cpu().numpy(), a_l)
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_lse_combine_kernel_against_oracle_partials(lib_bf16, oracle_mod, D):
+    """Step a4/a5 alone: oracle partials over disjoint key ranges, merged on the
+    GPU, must equal the oracle over all keys (includes -inf partials)."""
+    L, H = 500, 3
+    q, k, v = inputs.qkv(L, H, D, seed=31)
+    cuts = [0, 100, 101, 350, L]
+    parts = [oracle_mod.attention(q, k, v, True, key_range=(a, b)) for a, b in zip(cuts[:-1], cuts[1:])]
+    o_acc = torch.from_numpy(parts[0][0].astype(np.float32)).cuda()
+    l_acc = torch.from_numpy(parts[0][1].astype(np.float32)).cuda()
+    out = torch.empty((L, H, D), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((H, L), dtype=torch.float32, device="cuda")
+    for i, (po, pl) in enumerate(parts[1:], start=1):
+        dmha.lse_combine(o_acc, l_acc, torch.from_numpy(po.astype(np.float32)).cuda(),
+                         torch.from_numpy(pl.astype(np.float32)).cuda(), out, lse,
+                         final=(i == len(parts) - 1))
+    torch.cuda.synchronize()
+    ref_o, ref_l = oracle_mod.attention(q, k, v, True)
+    assert_parity(out.float().cpu().numpy(), lse.cpu().numpy(), ref_o, ref_l, "bf16", "combine")
+
+
+def test_attention_local_partial_with_global_positions(lib_bf16, oracle_mod):
+    """Step a2 alone on a (query chunk, key chunk) pair with zigzag-style maps:
+    fp32 partial output and -inf rows where no key is visible."""
+    L, H, D = 1024, 2, 64
+    q, k, v = inputs.qkv(L, H, D, seed=41)
+    # query rows: global [128,256) then [768,896); keys: global [256,512)
+    qidx = np.r_[128:256, 768:896]
+    kidx = np.r_[256:512]
+    out = torch.empty((len(qidx), H, D), dtype=torch.float32, device="cuda")
+    lse = torch.empty((H, len(qidx)), dtype=torch.float32, device="cuda")
+    dmha.attention_local(to_dev(q[qidx]), to_dev(k[kidx]), to_dev(v[kidx]), out, lse, causal=True,
+                         qmap=(128, 768, 128), kmap=(256, 512, 256), out_mode=1)
+    torch.cuda.synchronize()
+    ref_o, ref_l = oracle_mod.attention(q, k, v, True, rows=qidx, key_range=(256, 512))
+    o = out.cpu().numpy()
+    l = lse.cpu().numpy()
+    assert np.all(l[:, :128] == -np.inf) and np.all(o[:128] == 0)
+    assert_parity(o, l, ref_o, ref_l, "bf16", "local partial")
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_fp32_path_config_c1(oracle_mod, causal):
+    """C1: L=512, D=64, H=4, fp32, rel L2 <= 1e-4 (BASELINE.json configs[0])."""
+    ensure_lib("fp32")
+    if True:
+        L, H, D = 512, 4, 64
+        q, k, v = inputs.qkv(L, H, D, seed=1234, dtype="fp32")
+        out, lse = run_p1(q, k, v, causal, torch.float32)
+        ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+        assert_parity(out, lse, ref_o, ref_l, "fp32", f"C1 causal={causal}")
+        # fp32 ring emulation at P=4 as well
+        P = 4
+        parts = [np.stack([dmha.shard(x, P, r, "zigzag") for r in range(P)]) for x in (q, k, v)]
+        o4, l4 = dmha.forward_emulated(P, "zigzag", *(to_dev(p, torch.float32) for p in parts), L, causal)
+        torch.cuda.synchronize()
+        og = dmha.unshard(list(o4.cpu().numpy()), L, "zigzag")
+        lg = dmha.unshard([x.T for x in l4.cpu().numpy()], L, "zigzag").T
+        assert_parity(og, lg, ref_o, ref_l, "fp32", "C1 ring P=4")
+
+
+def test_error_codes(lib_bf16):
+    x = torch.zeros((64, 2, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(dmha.DmhaError) as e:
+        dmha.forward(x, x, x, 64, False, out=x)  # out aliases q
+    assert e.value.code == dmha.ERR_INVALID
+    y = torch.zeros((64, 2, 96), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(dmha.DmhaError) as e:
+        dmha.forward(y, y, y, 64, False)
+    assert e.value.code == dmha.ERR_UNSUPPORTED
+    with pytest.raises(dmha.DmhaError) as e:
+        dmha.forward_emulated(3, "contiguous", *(torch.zeros((3, 10, 2, 64), dtype=torch.bfloat16,
+                                                            device="cuda") for _ in range(3)), 31, False)
+    assert e.value.code == dmha.ERR_INVALID
