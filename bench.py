@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the distributed multi-head attention forward.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (N > 1)
+
+A step is one full dmha_forward (every hot-path row of SURVEY §8(a): shard
+map, ring K/V exchange, tcgen05 attention, LSE combine) over one batch of
+synthetic input.  Default workload C4 (BASELINE.json configs[3]): L=262144,
+D=128, H=16, bf16, non-causal, the sequence sharded over the N ranks
+(strong scaling; at N=1 it is the largest single-GPU config of the sweep).
+Metric: attention TFLOP/s = 4 L^2 D H (/2 causal) / time, whole job.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU fp64 oracle
+(oracle/, the tier's reference arm) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "C1": dict(L=512, D=64, H=4, causal=False, dtype="fp32", layout="contiguous",
+               desc="C1 single-head-group MHA L=512 D=64 H=4 fp32 non-causal"),
+    "C2": dict(L=16384, D=64, H=8, causal=False, dtype="bf16", layout="contiguous",
+               desc="C2 MHA L=16384 D=64 H=8 bf16 non-causal"),
+    "C2c": dict(L=16384, D=64, H=8, causal=True, dtype="bf16", layout="zigzag",
+                desc="C2 MHA L=16384 D=64 H=8 bf16 causal"),
+    "C3": dict(L=131072, D=128, H=8, causal=False, dtype="bf16", layout="contiguous",
+               desc="C3 MHA L=131072 D=128 H=8 bf16 sequence-sharded"),
+    "C4": dict(L=262144, D=128, H=16, causal=False, dtype="bf16", layout="contiguous",
+               desc="C4 MHA L=262144 D=128 H=16 bf16 strong-scaling sweep"),
+    "C5": dict(L=1048576, D=64, H=16, causal=True, dtype="bf16", layout="zigzag",
+               desc="C5 million-scale MHA L=1048576 D=64 H=16 bf16 causal"),
+}
+METRIC = "attention TFLOP/s (4*L^2*D*H, /2 causal)"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def flops(w) -> float:
+    f = 4.0 * w["L"] * w["L"] * w["D"] * w["H"]
+    return f / 2 if w["causal"] else f
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured (MEASURED_PEAKS.json)"
+    return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock / throttle reasons with NVML during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, torch_device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            pr = torch.cuda.get_device_properties(torch_device)
+            try:
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(torch_device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nv = pynvml
+        except Exception:
+            self._h = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self._h is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._h is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_sample(w, target_s: float = 12.0, seed: int = 4321):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
+    `n` query rows of one head against all L keys (same L, D; the per-row cost
+    is what the full job would pay L*H times).  Returns (TFLOP/s, cores, desc)."""
+    import numpy as np
+    from oracle import oracle
+    from synth import inputs
+    L, D = w["L"], w["D"]
+    q = inputs.normal((L, 1, D), seed, 0, w["dtype"])
+    k = inputs.normal((L, 1, D), seed, 1, w["dtype"])
+    v = inputs.normal((L, 1, D), seed, 2, w["dtype"])
+    q64, k64, v64 = (x.astype(np.float64) for x in (q, k, v))
+    rng = np.random.default_rng(seed)
+
+    def run(n):
+        rows = np.sort(rng.integers(0, L, n))
+        t0 = time.perf_counter()
+        oracle.attention(q64, k64, v64, w["causal"], rows=rows)
+        dt = time.perf_counter() - t0
+        keys = (rows + 1).sum() if w["causal"] else n * L
+        return 4.0 * keys * D / dt, dt
+
+    n = 16
+    rate, dt = run(n)
+    while dt < 0.5 and n < (1 << 20):
+        n *= 4
+        rate, dt = run(n)
+    n = max(1, int(n * target_s / max(dt, 1e-3)))
+    n = min(n, 1 << 22)
+    rate, dt = run(n)
+    desc = (f"{n} query rows x 1 head against all L={L} keys (D={D}, causal={w['causal']}), "
+            f"fp64 C/OpenMP oracle, {dt:.1f} s")
+    return rate / 1e12, oracle.num_threads(), desc, dt
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    oracle.build()
+    times, rates, desc, cores = [], [], "", 1
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for i in range(args.warmup + args.steps):
+        r, cores, desc, dt = cpu_oracle_sample(w, target_s=per_step, seed=9000 + i)
+        if i >= args.warmup:
+            rates.append(r)
+            times.append(dt)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, w),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(args, w):
+    return {"workload": w["desc"], "L": w["L"], "D": w["D"], "H": w["H"], "causal": w["causal"],
+            "layout": w["layout"], "batch": 1, "parallelism": f"seq-ring-cp{args.gpus}",
+            "l2": "inputs larger than L2 (q,k,v each >= 126 MB per rank)"
+            if w["L"] // args.gpus * w["H"] * w["D"] * 2 > 126e6 else
+            "L2 flushed (256 MB write) between timed steps"}
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, w):
+    import torch
+    import torch.distributed as dist
+    from paper_2302_06218_b200 import dmha
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L, D, H = w["L"], w["D"], w["H"]
+    if L % (2 * world if w["layout"] == "zigzag" else world):
+        raise SystemExit("L not divisible for this world size")
+    Lloc = L // world
+    tdt = torch.bfloat16 if w["dtype"] == "bf16" else torch.float32
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        dmha.init_distributed(w["dtype"], w["layout"], local)
+    else:
+        dmha.init(1, 0, None, local, w["dtype"], w["layout"], stream.cuda_stream)
+
+    gen = torch.Generator(device=dev)
+    shards = []
+    for tid in range(3):  # synthetic N(0,1) shards, seeded per (rank, tensor)
+        gen.manual_seed(1234 * 1000003 + rank * 101 + tid)
+        shards.append(torch.randn((Lloc, H, D), generator=gen, device=dev, dtype=torch.float32).to(tdt))
+    q, k, v = shards
+    out = torch.empty_like(q)
+    lse = torch.empty((H, Lloc), dtype=torch.float32, device=dev)
+    need_flush = Lloc * H * D * q.element_size() <= 126e6
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if need_flush else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        dmha.forward(q, k, v, L, w["causal"], out, lse)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: exactly K steps
+    st0 = dmha.get_stats()
+    dmha.set_profiling(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            dmha.forward(q, k, v, L, w["causal"], out, lse)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    st1 = dmha.get_stats()
+    dmha.set_profiling(False)
+    step_ms_local = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    step_ms = max_over_ranks(step_ms_local)
+    total_flops = flops(w)
+    value = total_flops / (step_ms / 1e3) / 1e12
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+
+    # ---- roofline of the dominant kernel (attention), event-timed per launch
+    peaks, peak_src = load_peaks()
+    attn_ms_avg = st1["attn_ms"] / max(1, st1["attn_launches"])
+    launches_per_step = st1["attn_launches"] / args.steps
+    flops_per_launch = total_flops / world / max(1.0, launches_per_step)
+    achieved = flops_per_launch / (attn_ms_avg / 1e3) / 1e12
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(args.workload)
+        except Exception:
+            traffic = None
+    attn_share = st1["attn_ms"] / args.steps / step_ms_local if step_ms_local > 0 else None
+    roofline = {"bound": "tensor", "kernel": f"attn_fwd_sm100_kernel<{D}>", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_kind": f"bf16 dense sustained, {peak_src}",
+                "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
+                "frac_of_datasheet_2250": achieved / 2250.0,
+                "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
+                "share_of_step": attn_share}
+    secondary = {}
+    if st1["combine_launches"]:
+        cm = st1["combine_ms"] / st1["combine_launches"]
+        cbytes = 12.0 * Lloc * H * D + 12.0 * Lloc * H
+        secondary["combine"] = {"bound": "hbm", "achieved": cbytes / (cm / 1e3) / 1e9,
+                                "peak": float(peaks.get("hbm_gbs", 6551.7)), "unit": "GB/s",
+                                "launch_ms": cm}
+        secondary["combine"]["frac"] = secondary["combine"]["achieved"] / secondary["combine"]["peak"]
+    if st1["exchanges"]:
+        xm = st1["exchange_ms"] / st1["exchanges"]
+        xbytes = 2.0 * Lloc * H * D * q.element_size()
+        secondary["exchange"] = {"bound": "nvlink", "achieved": xbytes / (xm / 1e3) / 1e9,
+                                 "peak": 770.0, "unit": "GB/s", "launch_ms": xm,
+                                 "note": "per-direction bytes sent per ring step / event time on the comm stream"}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+        hout = torch.empty(hq.shape, dtype=hq.dtype).pin_memory()
+        hlse = torch.empty((H, Lloc), dtype=torch.float32).pin_memory()
+        dmha.forward_host(hq, hk, hv, L, w["causal"], hout, hlse)  # warm the staging buffers
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            dmha.forward_host(hq, hk, hv, L, w["causal"], hout, hlse)
+        t_e2e = (time.perf_counter() - t0) / args.steps
+        barrier()
+        t_e2e = max_over_ranks(t_e2e)
+        e2e = {"value": total_flops / t_e2e / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 3 * hq.numel() * hq.element_size(),
+               "d2h_bytes_per_step": hout.numel() * hout.element_size() + hlse.numel() * 4,
+               "ms_per_step": 1e3 * t_e2e}
+
+    # ---- CPU oracle baseline (rank 0, N == 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, desc, _ = cpu_oracle_sample(w)
+        cpu = {"value": rate, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": w["dtype"], "data": "synthetic", "config": config_of(args, w),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "pct_of_peak": {"measured_sustained": value / (peak * world),
+                            "datasheet_2250": value / (2250.0 * world)},
+            "secondary": secondary or None,
+            "bytes_sent_per_step": (st1["bytes_sent"] - st0["bytes_sent"]) / args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    dmha.finalize()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and not os.environ.get("BENCH_ALLOW_SHORT_WARMUP"):
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+    return run_ours(args, w)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -21,7 +21,7 @@
  *   lse          : [H, L_loc] fp32 (natural log) — always fp32.
  * Element type of q/k/v/out is fixed by the dtype given to dmha_init:
  *   DMHA_BF16 -> bf16 storage, bf16 tensor-core MMA, fp32 accumulation/softmax;
- *   DMHA_FP32 -> fp32 storage (3xTF32 split on the tensor cores).
+ *   DMHA_FP32 -> fp32 storage and fp32 FMA-pipe arithmetic (SIMT kernel).
  *
  * Ownership: the caller owns q, k, v, out and lse.  q/k/v are read only (the
  * ring sends from them at step 0 and from library buffers afterwards); out and
@@ -68,6 +68,14 @@ struct dmha_stats {
   uint64_t forwards;        /* dmha_forward calls completed                      */
   uint64_t kernel_launches; /* device kernels launched by the library (cumulative) */
   uint64_t workspace_bytes; /* bytes currently held by the library on the device  */
+  /* Filled only while profiling is on (dmha_set_profiling): CUDA-event time of
+   * each launch, recorded on the stream the kernel runs on, summed. */
+  uint64_t attn_launches;    /* attention kernel launches timed                   */
+  uint64_t combine_launches; /* LSE-combine kernel launches timed                 */
+  uint64_t exchanges;        /* ring K/V exchanges (NCCL groups) timed            */
+  double attn_ms;            /* summed attention kernel time                      */
+  double combine_ms;         /* summed combine kernel time                        */
+  double exchange_ms;        /* summed send/recv time on the comm stream          */
 };
 
 /* ---- setup / teardown ---------------------------------------------------- */
@@ -126,7 +134,14 @@ int dmha_forward_emulated(int world_size, int layout, const void *q, const void 
  * world size and dtype (ring buffers + fp32 accumulators + staging excluded). */
 int dmha_workspace_bytes(int64_t L, int D, int H, size_t *bytes_out);
 
+/* Synchronises outstanding profiled work, then copies the counters. */
 int dmha_get_stats(struct dmha_stats *s);
+
+/* enable != 0: bracket every library kernel launch and ring exchange with CUDA
+ * events on its own stream and accumulate their durations into dmha_stats
+ * (measurement hook used by bench.py); enable == 0 stops it.  Also resets the
+ * timed counters. */
+int dmha_set_profiling(int enable);
 
 /* ---- individual hot-path steps (exported for tests and the bench) ------- */
 

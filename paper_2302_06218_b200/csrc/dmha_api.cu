@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/dmha.h"
 #include "kernels.h"
@@ -77,9 +78,61 @@ struct State {
   float* st_lse = nullptr;
   size_t st_bytes = 0, st_lse_elems = 0;
   dmha_stats stats{};
+  // profiling (dmha_set_profiling)
+  bool profile = false;
+  struct Rec {
+    cudaEvent_t a, b;
+    int kind;  // 0 attention, 1 combine, 2 exchange
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
 };
 
 State g;
+
+cudaEvent_t pool_event() {
+  if (!g.pool.empty()) {
+    cudaEvent_t e = g.pool.back();
+    g.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
+
+// Bracket the launches enqueued by `fn` on `stream` with profiling events.
+template <typename F>
+int timed(int kind, cudaStream_t stream, F&& fn) {
+  if (!g.profile) return fn();
+  cudaEvent_t a = pool_event(), b = pool_event();
+  if (a) cudaEventRecord(a, stream);
+  int rc = fn();
+  if (b) cudaEventRecord(b, stream);
+  if (a && b) g.pending.push_back({a, b, kind});
+  return rc;
+}
+
+void resolve_profiles() {
+  for (auto& r : g.pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.b) == cudaSuccess && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      if (r.kind == 0) {
+        g.stats.attn_ms += ms;
+        g.stats.attn_launches++;
+      } else if (r.kind == 1) {
+        g.stats.combine_ms += ms;
+        g.stats.combine_launches++;
+      } else {
+        g.stats.exchange_ms += ms;
+        g.stats.exchanges++;
+      }
+    }
+    g.pool.push_back(r.a);
+    g.pool.push_back(r.b);
+  }
+  g.pending.clear();
+}
 
 size_t elem_bytes(int dtype) { return dtype == DMHA_BF16 ? 2 : 4; }
 
@@ -233,8 +286,12 @@ int run_local(const void* q, const void* k, const void* v, void* out, float* lse
   a.qmap = qm;
   a.kmap = km;
   a.out_mode = out_mode;
-  cudaError_t e = g.dtype == DMHA_BF16 ? dmha::launch_attn_fwd_bf16(a, g.stream)
-                                       : dmha::launch_attn_fwd_fp32(a, g.stream);
+  cudaError_t e = cudaSuccess;
+  timed(0, g.stream, [&]() {
+    e = g.dtype == DMHA_BF16 ? dmha::launch_attn_fwd_bf16(a, g.stream)
+                             : dmha::launch_attn_fwd_fp32(a, g.stream);
+    return 0;
+  });
   if (e != cudaSuccess)
     return fail(DMHA_ERR_CUDA, "dmha: attention kernel launch failed: %s", cudaGetErrorString(e));
   g.stats.kernel_launches += dmha::attn_launches_per_call();
@@ -243,8 +300,12 @@ int run_local(const void* q, const void* k, const void* v, void* out, float* lse
 
 int run_combine(float* o_part, float* lse_part, void* out, float* lse, int64_t Lq, int D, int H,
                 int final_step) {
-  cudaError_t e = dmha::launch_lse_combine(g.o_acc, g.lse_acc, o_part, lse_part, out, lse, Lq,
-                                           D, H, final_step, g.dtype == DMHA_BF16, g.stream);
+  cudaError_t e = cudaSuccess;
+  timed(1, g.stream, [&]() {
+    e = dmha::launch_lse_combine(g.o_acc, g.lse_acc, o_part, lse_part, out, lse, Lq, D, H,
+                                 final_step, g.dtype == DMHA_BF16, g.stream);
+    return 0;
+  });
   if (e != cudaSuccess)
     return fail(DMHA_ERR_CUDA, "dmha: combine launch failed: %s", cudaGetErrorString(e));
   g.stats.kernel_launches += 1;
@@ -361,6 +422,9 @@ int dmha_finalize(void) {
   free_ptr(g.st_qkv);
   free_ptr(g.st_out);
   free_ptr(g.st_lse);
+  resolve_profiles();
+  for (cudaEvent_t e : g.pool) cudaEventDestroy(e);
+  g.pool.clear();
   if (g.nccl) ncclCommDestroy(g.nccl);
   cudaEvent_t evs[6] = {g.ev_start, g.ev_comm_end, g.ev_recv[0], g.ev_recv[1], g.ev_done[0],
                         g.ev_done[1]};
@@ -386,7 +450,17 @@ int dmha_workspace_bytes(int64_t L, int D, int H, size_t* bytes_out) {
 
 int dmha_get_stats(dmha_stats* s) {
   if (!s) return fail(DMHA_ERR_INVALID, "dmha_get_stats: null");
+  resolve_profiles();
   *s = g.stats;
+  return DMHA_OK;
+}
+
+int dmha_set_profiling(int enable) {
+  if (int rc = check_state()) return rc;
+  resolve_profiles();
+  g.profile = enable != 0;
+  g.stats.attn_launches = g.stats.combine_launches = g.stats.exchanges = 0;
+  g.stats.attn_ms = g.stats.combine_ms = g.stats.exchange_ms = 0.0;
   return DMHA_OK;
 }
 
@@ -429,12 +503,16 @@ int dmha_forward(const void* q, const void* k, const void* v, void* out, float* 
       const int nb = (s + 1) & 1;
       if (s >= 2) CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_done[nb], 0));
       char* dst = static_cast<char*>(g.kvbuf[nb]);
-      CK_NCCL(ncclGroupStart());
-      CK_NCCL(ncclSend(kcur, blk, ncclChar, next, g.nccl, g.comm));
-      CK_NCCL(ncclSend(vcur, blk, ncclChar, next, g.nccl, g.comm));
-      CK_NCCL(ncclRecv(dst, blk, ncclChar, prev, g.nccl, g.comm));
-      CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, prev, g.nccl, g.comm));
-      CK_NCCL(ncclGroupEnd());
+      int rc = timed(2, g.comm, [&]() {
+        CK_NCCL(ncclGroupStart());
+        CK_NCCL(ncclSend(kcur, blk, ncclChar, next, g.nccl, g.comm));
+        CK_NCCL(ncclSend(vcur, blk, ncclChar, next, g.nccl, g.comm));
+        CK_NCCL(ncclRecv(dst, blk, ncclChar, prev, g.nccl, g.comm));
+        CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, prev, g.nccl, g.comm));
+        CK_NCCL(ncclGroupEnd());
+        return static_cast<int>(DMHA_OK);
+      });
+      if (rc) return rc;
       CK_CUDA(cudaEventRecord(g.ev_recv[nb], g.comm));
       g.stats.bytes_sent += 2 * blk;
     }

@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "dmha_get_unique_id", "dmha_init", "dmha_set_stream", "dmha_finalize", "dmha_last_error",
     "dmha_forward", "dmha_forward_host", "dmha_forward_emulated", "dmha_workspace_bytes",
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
-    "dmha_synchronize",
+    "dmha_synchronize", "dmha_set_profiling",
 )
 
 
@@ -39,7 +39,10 @@ class DmhaError(RuntimeError):
 class Stats(ctypes.Structure):
     _fields_ = [("bytes_sent", ctypes.c_uint64), ("ring_steps", ctypes.c_uint64),
                 ("forwards", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
-                ("workspace_bytes", ctypes.c_uint64)]
+                ("workspace_bytes", ctypes.c_uint64), ("attn_launches", ctypes.c_uint64),
+                ("combine_launches", ctypes.c_uint64), ("exchanges", ctypes.c_uint64),
+                ("attn_ms", ctypes.c_double), ("combine_ms", ctypes.c_double),
+                ("exchange_ms", ctypes.c_double)]
 
 
 _lib = None
@@ -67,6 +70,7 @@ def lib():
             "dmha_attention_local": [P, P, P, P, P, I64, I64, I, I, I, I64, I64, I64, I64, I64, I64, I],
             "dmha_lse_combine": [P, P, P, P, P, P, I64, I, I, I],
             "dmha_synchronize": [],
+            "dmha_set_profiling": [I],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -221,7 +225,11 @@ def workspace_bytes(L: int, D: int, H: int) -> int:
 def get_stats() -> dict:
     s = Stats()
     _check(lib().dmha_get_stats(ctypes.byref(s)))
-    return {f: int(getattr(s, f)) for f, _ in Stats._fields_}
+    return {f: (float if t is ctypes.c_double else int)(getattr(s, f)) for f, t in Stats._fields_}
+
+
+def set_profiling(enable: bool):
+    _check(lib().dmha_set_profiling(int(bool(enable))))
 
 
 def local_to_global(L: int, world_size: int, rank: int, layout, i: int) -> int:
