@@ -11,18 +11,25 @@
 // both shard layouts.  S, P and O never leave the SM: S and O accumulate in
 // TMEM, P is written back to TMEM as bf16 and consumed from there.
 //
-// CTA = 2 query tiles of 128 rows (256 rows) of one head; 12 warps:
-//   warps 0-3  softmax for Q tile 0 (thread t <-> TMEM lane t <-> row t)
-//   warps 4-7  softmax for Q tile 1
-//   warp  8    TMA producer (Q once; K_j, V_j through an NST-slot ring)
-//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 10-11 idle (keep the CTA at 3 warpgroups)
+// CTA = 2 query tiles of 128 rows (256 rows) of one head; 20 warps:
+//   warps 0-15  softmax: warpgroup w = warp/4 handles Q tile g = w/2 and score
+//               columns [64h, 64h+64) with h = w%2 (two warpgroups share each
+//               row: thread t <-> TMEM lane t <-> row t; the row max is
+//               exchanged through shared memory once per KV tile)
+//   warp  16    TMA producer (Q once; K_j, V_j through an NST-slot ring)
+//   warp  17    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 18-19 idle (keep the CTA at whole warpgroups for setmaxnreg)
+// Splitting each row over two warpgroups halves the softmax latency, which is
+// the serial part of every tile: S_g(j+1) cannot start before PV_g(j) has read
+// P_g(j) (they share TMEM columns), so per Q tile the loop is
+// softmax -> PV + QK^T -> softmax, and the two Q tiles ping-pong on the tensor
+// core.  (Timeline measured with dmha_debug_set_trace.)
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D);
-// P_g (bf16x2) aliases the first 64 columns of S_g.
+// P_g (bf16x2) aliases the first 64 columns of S_g (half h writes [32h,32h+32)).
 // MMA order per KV tile j:  PV0_{j-1}, S0_j, PV1_{j-1}, S1_j — S_g(j) is issued
 // after PV_g(j-1) read P_g(j-1) (tcgen05.mma executes in issue order), and the
 // commit that signals S_g(j) also covers PV_g(j-1), so the softmax warps can
-// rescale O_g right after they see S_g(j).
+// rescale O_g right after they see S_g(j) (warpgroup h = 0 does it).
 // Online softmax in the exp2 domain with a stale running max: O is rescaled
 // only when the tile max exceeds the running max by more than 8 (factor 256);
 // exact because l and O always share the max that was subtracted.
@@ -33,19 +40,27 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx_sm100.cuh"
 
 namespace dmha {
+extern unsigned long long* g_trace;
 namespace {
 
 constexpr int kBM = 128;          // query rows per tile (MMA M)
 constexpr int kBN = 128;          // keys per tile (MMA N of QK^T, K of PV)
-constexpr int kThreads = 384;     // 12 warps
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
+constexpr int kSoftmaxWarps = 16;
+constexpr int kThreads = 640;     // 20 warps
+constexpr int kProducerWarp = 16;
+constexpr int kMmaWarp = 17;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
+// Register split (65536 per SM, 1 CTA/SM, 96 per thread at launch): the control
+// warpgroup (TMA, MMA, 2 idle warps) gives registers to the four softmax
+// warpgroups: 4*104 + 56 <= 512.
+constexpr uint32_t kRegsCtl = 56;
+constexpr uint32_t kRegsSoftmax = 104;
 
 template <int D>
 struct Cfg {
@@ -55,8 +70,13 @@ struct Cfg {
   static constexpr int kStages = (D == 128) ? 4 : 6;        // K/V ring slots
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = 2 * kTileBytes;
-  static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
+  static constexpr int kRedOff = kKVOff + kStages * kTileBytes;  // row-max exchange [2][2][128] f32
+  static constexpr int kBarOff = kRedOff + 2 * 2 * 128 * 4;
   static constexpr int kSmemBytes = kBarOff + 256 + 1024;   // + barriers + align slack
+  // Default number (of every 8) of score-column pairs whose exp2 runs as a
+  // polynomial on the FMA pipe instead of MUFU (D=64 has half the MMA work
+  // per exponential of D=128).  Overridable per launch for measurement.
+  static constexpr int kEmuDefault = (D == 128) ? 2 : 4;
   static constexpr uint32_t kIdescQK = ptx::make_idesc(1, kBM, kBN, 0, 0);
   static constexpr uint32_t kIdescPV = ptx::make_idesc(1, kBM, D, 0, 1);  // V is MN-major
 };
@@ -71,7 +91,78 @@ struct Params {
   float* lse;
   int out_mode;
   int n_mblk;
+  unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
+
+// Timeline trace (measurement hook): clock64 stamps for the first kTraceCtas
+// CTAs of head 0 and their first kTraceTiles KV tiles.  Events:
+//  0/2: softmax WG0/WG1 saw S full   1/3: WG0/WG1 arrive P ready
+//  4/5: MMA warp saw P0/P1 ready     6: MMA warp issued S1(j+1)
+constexpr int kTraceCtas = 4, kTraceEvents = 7, kTraceTiles = 64;
+__device__ __forceinline__ void trace_stamp(const Params& p, int ev, int j) {
+  if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < kTraceCtas && j < kTraceTiles)
+    p.trace[(blockIdx.x * kTraceEvents + ev) * kTraceTiles + j] = clock64();
+}
+
+// 2^x for a pair on MUFU.EX2.
+__device__ __forceinline__ float2 exp2_mufu2(float2 x) {
+  return make_float2(ptx::ex2_approx(x.x), ptx::ex2_approx(x.y));
+}
+
+// 2^x for a pair on the FMA pipe (FADD2/FFMA2 + 2 ALU ops per element):
+// n = round(x) via the 1.5*2^23 magic add, f = x - n in [-0.5, 0.5],
+// 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5, below the
+// 2^-9 bf16 rounding P gets anyway), exponent added as (n << 23).
+// x is clamped at -126 so -inf (masked) gives ~0 and the exponent cannot wrap.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+  float2 p = __ffma2_rn(f, make_float2(0.055171459913253784f, 0.055171459913253784f),
+                        make_float2(0.2426108568906784f, 0.2426108568906784f));
+  p = __ffma2_rn(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
+  p = __ffma2_rn(p, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
+  const uint32_t rx = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+  const uint32_t ry = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+  return make_float2(__uint_as_float(rx), __uint_as_float(ry));
+}
+
+// P = exp2(S*scale*log2e - m) for this thread's 64 score columns, packed to
+// bf16 and written to its 32 P columns in TMEM (16-column chunks, so the fp32
+// scores die as P is produced).  Returns the fp32 sum of the 64 P values.
+// EMU of every 8 column pairs use exp2_poly2 (FMA pipe), the rest MUFU.
+template <int EMU>
+__device__ __forceinline__ float exp_tile(float (&s)[64], float sl2, float m_use, uint32_t tP) {
+  const float2 sc2 = make_float2(sl2, sl2);
+  const float2 nm2 = make_float2(-m_use, -m_use);
+  float2 sum_a = make_float2(0.f, 0.f), sum_b = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      // x = S*scale*log2e - m on the packed FP32x2 pipe (FFMA2)
+      const float2 x = __ffma2_rn(make_float2(s[32 * c + 2 * e], s[32 * c + 2 * e + 1]), sc2, nm2);
+      const float2 pe = (((c * 16 + e) & 7) < EMU) ? exp2_poly2(x) : exp2_mufu2(x);
+      if (e & 1)
+        sum_b = __fadd2_rn(sum_b, pe);
+      else
+        sum_a = __fadd2_rn(sum_a, pe);
+      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
+      pk[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    ptx::tmem_st16(tP + c * 16, pk);
+  }
+  return (sum_a.x + sum_a.y) + (sum_b.x + sum_b.y);
+}
+
+// Named barrier over the 256 threads (two warpgroups) that share Q tile g.
+__device__ __forceinline__ void pair_sync(int g) {
+  asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+}
 
 __device__ __forceinline__ int64_t pos_of(const PosMap& m, int64_t i) {
   return i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
@@ -102,7 +193,7 @@ __device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
   return static_cast<int>((lim + kBN - 1) / kBN);
 }
 
-template <int D>
+template <int D, int kEmu, bool kRegSplit>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
@@ -113,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem + C::kQOff;
   uint8_t* sKV = smem + C::kKVOff;
+  float* red = reinterpret_cast<float*>(smem + C::kRedOff);  // [g][h][row]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;
@@ -139,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int g = 0; g < 2; ++g) {
       ptx::mbar_init(&s_full[g], 1);
-      ptx::mbar_init(&p_ready[g], kBM);
+      ptx::mbar_init(&p_ready[g], 2 * kBM);  // both column halves of every row
       ptx::mbar_init(&o_final[g], 1);
     }
     ptx::fence_mbar_init();
@@ -155,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
+    if (kRegSplit) ptx::setmaxnreg_dec<kRegsCtl>();
     if (lane == 0 && nkv > 0) {
       ptx::mbar_arrive_expect_tx(q_full, 2 * C::kTileBytes);
       for (int g = 0; g < 2; ++g)
@@ -177,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    if (kRegSplit) ptx::setmaxnreg_dec<kRegsCtl>();
     if (lane == 0 && nkv > 0) {
       const uint32_t sq = ptx::smem_u32(sQ);
       const uint32_t skv = ptx::smem_u32(sKV);
@@ -227,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
         ptx::mbar_wait(&p_ready[0], ppar);
+        trace_stamp(p, 4, j - 1);
         ptx::tc_fence_after();
         pv(0, slotV, j > 1);
         if (more) {
@@ -236,12 +331,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mma_commit(&o_final[0]);
         }
         ptx::mbar_wait(&p_ready[1], ppar);
+        trace_stamp(p, 5, j - 1);
         ptx::tc_fence_after();
         pv(1, slotV, j > 1);
         ptx::mma_commit(&kv_empty[slotV]);
         if (more) {
           qk(1, slotK2);
           ptx::mma_commit(&s_full[1]);
+          trace_stamp(p, 6, j);
           ptx::mma_commit(&kv_empty[slotK2]);
         } else {
           ptx::mma_commit(&o_final[1]);
@@ -249,9 +346,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
+  } else if (warp >= kSoftmaxWarps) {
+    if (kRegSplit) ptx::setmaxnreg_dec<kRegsCtl>();  // idle warps of the control warpgroup
+  } else {
     // ------------------------------------------------------------ softmax
-    const int g = warp >> 2;                  // Q tile of this warpgroup
+    if (kRegSplit) ptx::setmaxnreg_inc<kRegsSoftmax>();
+    const int wg = warp >> 2;
+    const int g = wg >> 1;                    // Q tile of this warpgroup
+    const int h = wg & 1;                     // score-column half / output-column half
     const int quarter = warp & 3;             // TMEM lane quarter
     const int r = quarter * 32 + lane;        // row within the tile
     const int64_t row = m0 + g * kBM + r;     // local query row
@@ -259,38 +361,49 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t qp = pos_of(p.qmap, row_ok ? row : p.Lq - 1);
     const int64_t klim = key_limit(p, qp);
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + g * kBN;
+    const uint32_t tS = tmem + lane_addr + g * kBN + h * 64;  // this half's 64 score columns
+    const uint32_t tP = tmem + lane_addr + g * kBN + h * 32;  // this half's 32 P columns
     const uint32_t tO = tmem + lane_addr + 256 + g * 128;
+    float* red_mine = red + (g * 2 + h) * kBM + r;
+    const float* red_other = red + (g * 2 + (h ^ 1)) * kBM + r;
     const float sl2 = p.scale_log2;
+    const bool leader = (threadIdx.x % 256) == 0;  // one stamp per Q tile
 
-    float m_run = -INFINITY;  // running max, log2 units (scaled)
-    float l_run = 0.f;
+    float m_run = -INFINITY;  // running max, log2 units (scaled); equal in both halves
+    float l_run = 0.f;        // this half's share of the row sum
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(&s_full[g], static_cast<uint32_t>(j & 1));
+      if (leader) trace_stamp(p, 2 * g, j);
       ptx::tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
+      float s[64];
+      ptx::tmem_ld32(tS, *reinterpret_cast<float(*)[32]>(&s[0]));
+      ptx::tmem_ld32(tS + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
       ptx::tmem_wait_ld();
 
-      int64_t nv64 = klim - static_cast<int64_t>(j) * kBN;
-      const int nvalid = nv64 < 0 ? 0 : (nv64 > kBN ? kBN : static_cast<int>(nv64));
-      if (!__all_sync(0xffffffffu, nvalid >= kBN)) {
+      const int64_t nv64 = klim - static_cast<int64_t>(j) * kBN - h * 64;
+      const int nvalid = nv64 < 0 ? 0 : (nv64 > 64 ? 64 : static_cast<int>(nv64));
+      // Warp-uniform in both halves of a row: masked iff any row of the Q tile
+      // has fewer than all 128 keys of the tile visible.
+      const bool masked = !__all_sync(0xffffffffu, klim - static_cast<int64_t>(j) * kBN >= kBN);
+      if (masked) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
+        for (int c = 0; c < 64; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
       float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
 #pragma unroll
-      for (int c = 4; c < 128; c += 4) {
+      for (int c = 4; c < 64; c += 4) {
         mx0 = fmaxf(mx0, s[c]);
         mx1 = fmaxf(mx1, s[c + 1]);
         mx2 = fmaxf(mx2, s[c + 2]);
         mx3 = fmaxf(mx3, s[c + 3]);
       }
-      const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const float pmax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+      *red_mine = pmax;
+      pair_sync(g);  // the other half reads this slot before tile j+1 can be
+                     // written: S_g(j+1) needs both halves' P_g(j) first.
+      const float mt = fmaxf(pmax, *red_other) * sl2;
       const bool need = mt > m_run + kRescaleThreshold;
-      const bool warp_rescale = __any_sync(0xffffffffu, need);
+      const bool warp_rescale = __any_sync(0xffffffffu, need);  // same in both halves
       float alpha = 1.f;
       if (warp_rescale) {
         const float m_new = fmaxf(m_run, mt);
@@ -298,28 +411,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run *= alpha;
         m_run = m_new;
       }
-      // P = exp2(S*scale*log2e - m) -> bf16, written over the first 64 columns
-      // of S in 16-column chunks so the fp32 scores die as P is produced.
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float sum0 = 0.f, sum1 = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], sl2, -m_use));
-          const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], sl2, -m_use));
-          sum0 += e0;
-          sum1 += e1;
-          __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
-          pk[e] = *reinterpret_cast<uint32_t*>(&b);
-        }
-        ptx::tmem_st16(tS + c * 16, pk);
-      }
-      l_run += sum0 + sum1;
+      // Unmasked tiles send kEmu of every 8 column pairs to the FMA-pipe
+      // polynomial; masked tiles (-inf entries, must give exactly 0) use MUFU only.
+      if (masked)
+        l_run += exp_tile<0>(s, sl2, m_use, tP);
+      else
+        l_run += exp_tile<kEmu>(s, sl2, m_use, tP);
       // O_g holds PV_g(j-1) (complete: covered by the S_g(j) commit) and PV_g(j)
       // is not issued before p_ready, so O can be rescaled in place here.
-      if (warp_rescale && j > 0) {
+      if (warp_rescale && j > 0 && h == 0) {
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           float o[32];
@@ -332,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
+      if (leader) trace_stamp(p, 2 * g + 1, j);
       ptx::mbar_arrive(&p_ready[g]);
     }
     if (nkv > 0) {
@@ -339,17 +441,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
     }
     // ---------------------------------------------------------- epilogue
-    const bool empty = !(l_run > 0.f);
-    const float inv_l = empty ? 0.f : 1.f / l_run;
-    if (row_ok)
+    // Row sum = both halves' shares (same m_run); each half writes D/2 columns.
+    *red_mine = l_run;
+    pair_sync(g);
+    const float l_tot = l_run + *red_other;
+    const bool empty = !(l_tot > 0.f);
+    const float inv_l = empty ? 0.f : 1.f / l_tot;
+    if (row_ok && h == 0)
       p.lse[static_cast<int64_t>(head) * p.Lq + row] =
-          empty ? -INFINITY : (m_run + __log2f(l_run)) * 0.69314718055994530942f;
-    const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D);
+          empty ? -INFINITY : (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
+    const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D) + h * (D / 2);
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < D / 64; ++c) {
       float o[32];
       if (nkv > 0) {
-        ptx::tmem_ld32(tO + c * 32, o);
+        ptx::tmem_ld32(tO + h * (D / 2) + c * 32, o);
         ptx::tmem_wait_ld();
       } else {
 #pragma unroll
@@ -426,21 +532,46 @@ bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
   return r == CUDA_SUCCESS;
 }
 
+// Kernel variant (measurement knob): DMHA_EMU=<pairs of 8 on the FMA pipe>,
+// DMHA_REGSPLIT=0/1.  Defaults: Cfg<D>::kEmuDefault, register split on.
+struct Variant {
+  int emu;
+  bool regsplit;
+};
+
 template <int D>
-cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
+Variant variant() {
+  static Variant v = [] {
+    Variant x{Cfg<D>::kEmuDefault, true};
+    if (const char* e = std::getenv("DMHA_EMU")) x.emu = std::atoi(e);
+    if (const char* r = std::getenv("DMHA_REGSPLIT")) x.regsplit = std::atoi(r) != 0;
+    return x;
+  }();
+  return v;
+}
+
+template <int D, int E, bool R>
+cudaError_t launch_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                     const Params& p, dim3 grid, cudaStream_t stream) {
   using C = Cfg<D>;
-  CUtensorMap tq, tk, tv;
-  if (!make_map(&tq, a.q, a.Lq, a.H, D) || !make_map(&tk, a.k, a.Lk, a.H, D) ||
-      !make_map(&tv, a.v, a.Lk, a.H, D))
-    return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, R>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  attn_fwd_sm100_kernel<D, E, R><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
+  CUtensorMap tq, tk, tv;
+  if (!make_map(&tq, a.q, a.Lq, a.H, D) || !make_map(&tk, a.k, a.Lk, a.H, D) ||
+      !make_map(&tv, a.v, a.Lk, a.H, D))
+    return cudaErrorInvalidValue;
   Params p;
   p.Lq = a.Lq;
   p.Lk = a.Lk;
@@ -453,12 +584,23 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   p.lse = a.lse;
   p.out_mode = a.out_mode;
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
+  p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H);
-  attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
-  return cudaGetLastError();
+  const Variant v = variant<D>();
+  if (!v.regsplit) return launch_v<D, Cfg<D>::kEmuDefault, false>(tq, tk, tv, p, grid, stream);
+  switch (v.emu) {
+    case 0: return launch_v<D, 0, true>(tq, tk, tv, p, grid, stream);
+    case 1: return launch_v<D, 1, true>(tq, tk, tv, p, grid, stream);
+    case 2: return launch_v<D, 2, true>(tq, tk, tv, p, grid, stream);
+    case 3: return launch_v<D, 3, true>(tq, tk, tv, p, grid, stream);
+    case 4: return launch_v<D, 4, true>(tq, tk, tv, p, grid, stream);
+    default: return launch_v<D, Cfg<D>::kEmuDefault, true>(tq, tk, tv, p, grid, stream);
+  }
 }
 
 }  // namespace
+
+unsigned long long* g_trace = nullptr;
 
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream) {
   if (a.Lq <= 0) return cudaSuccess;

@@ -638,6 +638,11 @@ int dmha_lse_combine(float* o_acc, float* lse_acc, const float* o_part, const fl
   return DMHA_OK;
 }
 
+int dmha_debug_set_trace(void* dev_buf) {
+  dmha::g_trace = static_cast<unsigned long long*>(dev_buf);
+  return DMHA_OK;
+}
+
 int dmha_synchronize(void) {
   if (int rc = check_state()) return rc;
   CK_CUDA(cudaStreamSynchronize(g.stream));

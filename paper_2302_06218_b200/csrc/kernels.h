@@ -40,6 +40,9 @@ cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part
                                int D, int H, int final_step, int out_dtype_bf16,
                                cudaStream_t stream);
 
+// Debug timeline buffer for the bf16 attention kernel (null = off).
+extern unsigned long long* g_trace;
+
 // Number of kernel launches a call of launch_attn_fwd_* makes (for stats).
 inline int attn_launches_per_call() { return 1; }
 

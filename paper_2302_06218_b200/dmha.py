@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "dmha_get_unique_id", "dmha_init", "dmha_set_stream", "dmha_finalize", "dmha_last_error",
     "dmha_forward", "dmha_forward_host", "dmha_forward_emulated", "dmha_workspace_bytes",
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
-    "dmha_synchronize", "dmha_set_profiling",
+    "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace",
 )
 
 
@@ -71,6 +71,7 @@ def lib():
             "dmha_lse_combine": [P, P, P, P, P, P, I64, I, I, I],
             "dmha_synchronize": [],
             "dmha_set_profiling": [I],
+            "dmha_debug_set_trace": [P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -226,6 +227,11 @@ def get_stats() -> dict:
     s = Stats()
     _check(lib().dmha_get_stats(ctypes.byref(s)))
     return {f: (float if t is ctypes.c_double else int)(getattr(s, f)) for f, t in Stats._fields_}
+
+
+def debug_set_trace(buf):
+    """Timeline hook: buf = device uint64 tensor of >= 4*7*64 entries, or None."""
+    _check(lib().dmha_debug_set_trace(None if buf is None else _ptr(buf)))
 
 
 def set_profiling(enable: bool):

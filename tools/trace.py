@@ -1,0 +1,34 @@
+"""Kernel timeline: run one forward with the trace hook and print per-tile
+softmax / MMA phase durations (SM cycles) for the first traced CTA."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2302_06218_b200 import dmha  # noqa: E402
+
+L = int(os.environ.get("TL", 262144 // 8)); H = 16; D = int(os.environ.get("TD", 128))
+dmha.init(1, 0, None, 0, "bf16", "contiguous")
+q, k, v = (torch.randn(L, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
+buf = torch.zeros(4 * 7 * 64, dtype=torch.int64, device="cuda")
+dmha.forward(q, k, v, L, False)
+dmha.debug_set_trace(buf)
+dmha.forward(q, k, v, L, False)
+torch.cuda.synchronize()
+dmha.debug_set_trace(None)
+t = buf.view(4, 7, 64).cpu().numpy().astype(np.int64)
+for c in range(2):
+    tc = t[c] - t[c][0][0]
+    print(f"CTA {c}: event rows (cycles rel. to WG0 first S): 0=S0 1=P0 2=S1 3=P1 4=mmaP0 5=mmaP1 6=mmaS1next")
+    for j in range(8, 16):
+        print(j, " ".join(f"{tc[e][j]:8d}" for e in range(7)))
+    # steady-state stats over tiles 8..60
+    js = range(8, 60)
+    per = np.diff(tc[0][8:60]).mean()
+    sm0 = np.mean([tc[1][j] - tc[0][j] for j in js]); sm1 = np.mean([tc[3][j] - tc[2][j] for j in js])
+    w0 = np.mean([tc[0][j + 1] - tc[1][j] for j in js]); w1 = np.mean([tc[2][j + 1] - tc[3][j] for j in js])
+    lat0 = np.mean([tc[4][j] - tc[1][j] for j in js])
+    print(f"  period/tile {per:.0f}  softmax0 {sm0:.0f}  softmax1 {sm1:.0f}  wait-S0 {w0:.0f}  wait-S1 {w1:.0f}  P0->mma-sees {lat0:.0f}")
+dmha.finalize()
