@@ -11,28 +11,30 @@
 // both shard layouts.  S, P and O never leave the SM: S and O accumulate in
 // TMEM, P is written back to TMEM as bf16 and consumed from there.
 //
-// CTA = 2 query tiles of 128 rows (256 rows) of one head; 20 warps:
-//   warps 0-15  softmax: warpgroup w = warp/4 handles Q tile g = w/2 and score
-//               columns [64h, 64h+64) with h = w%2 (two warpgroups share each
-//               row: thread t <-> TMEM lane t <-> row t; the row max is
-//               exchanged through shared memory once per KV tile)
-//   warp  16    TMA producer (Q once; K_j, V_j through an NST-slot ring)
-//   warp  17    TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 18-19 idle (keep the CTA at whole warpgroups for setmaxnreg)
-// Splitting each row over two warpgroups halves the softmax latency, which is
-// the serial part of every tile: S_g(j+1) cannot start before PV_g(j) has read
-// P_g(j) (they share TMEM columns), so per Q tile the loop is
-// softmax -> PV + QK^T -> softmax, and the two Q tiles ping-pong on the tensor
-// core.  (Timeline measured with dmha_debug_set_trace.)
-// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D);
-// P_g (bf16x2) aliases the first 64 columns of S_g (half h writes [32h,32h+32)).
-// MMA order per KV tile j:  PV0_{j-1}, S0_j, PV1_{j-1}, S1_j — S_g(j) is issued
-// after PV_g(j-1) read P_g(j-1) (tcgen05.mma executes in issue order), and the
-// commit that signals S_g(j) also covers PV_g(j-1), so the softmax warps can
-// rescale O_g right after they see S_g(j) (warpgroup h = 0 does it).
-// Online softmax in the exp2 domain with a stale running max: O is rescaled
-// only when the tile max exceeds the running max by more than 8 (factor 256);
-// exact because l and O always share the max that was subtracted.
+// Structure:
+//  * CTA = one 128-row query tile of one head; CTAs run in clusters of 2 that
+//    work on adjacent query tiles of the same head and share every K/V tile:
+//    each CTA TMA-loads half of the tile's rows and multicasts it into both
+//    CTAs' shared memory, so L2 -> SM traffic is one K/V tile per 256 rows.
+//  * S is triple-buffered in TMEM, so QK^T of tiles j+1, j+2 runs on the
+//    tensor core while the softmax of tile j runs; the per-tile loop is bounded
+//    by max(tensor core, softmax) instead of their sum (the single-buffer
+//    design measured ~3300 cycles/tile for 2048 cycles of MMA).
+//  * 12 warps: 0-7 softmax (warpgroup w owns the KV tiles j = w mod 2 and
+//    S buffer w; thread t <-> TMEM lane t <-> row t, a full 128-column score
+//    row per thread; only the running max is handed between the warpgroups),
+//    8 TMA producer, 9 TMEM allocator + tcgen05.mma issuer (whole warp,
+//    elect.sync issues), 10-11 idle.
+//  * TMEM (512 cols): S buffers [0,128), [128,256), [256,384); O [384, 384+D).
+//    P(j) (bf16x2) overwrites the first 64 columns of S buffer j%3.
+//  * MMA issue order (tcgen05.mma executes in order): S(0), S(1), S(2), then
+//    per tile j: PV(j) [after P(j) ready], S(j+3) into the buffer PV(j) just
+//    read.  K/V ring slots are loaded in exactly this order (K0 K1 K2 V0 K3 V1
+//    K4 ...).
+//  * Online softmax in the exp2 domain with a stale running max: O is rescaled
+//    only when the tile max exceeds the running max by more than 8 (factor
+//    256) — exact because l and O always share the subtracted max.  The rare
+//    rescale first waits for PV(j-1) (pv_done barrier).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -49,34 +51,31 @@ namespace dmha {
 extern unsigned long long* g_trace;
 namespace {
 
-constexpr int kBM = 128;          // query rows per tile (MMA M)
+constexpr int kBM = 128;          // query rows per CTA (MMA M)
 constexpr int kBN = 128;          // keys per tile (MMA N of QK^T, K of PV)
-constexpr int kSoftmaxWarps = 16;
-constexpr int kThreads = 640;     // 20 warps
-constexpr int kProducerWarp = 16;
-constexpr int kMmaWarp = 17;
+constexpr int kThreads = 384;     // 12 warps
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
-// Register split (65536 per SM, 1 CTA/SM, 96 per thread at launch): the control
-// warpgroup (TMA, MMA, 2 idle warps) gives registers to the four softmax
-// warpgroups: 4*104 + 56 <= 512.
-constexpr uint32_t kRegsCtl = 56;
-constexpr uint32_t kRegsSoftmax = 104;
+constexpr int kNB = 3;            // S buffers in TMEM (S(t+3) reuses buffer t%3 after PV(t))
+constexpr int kOCol = kNB * kBN;  // first TMEM column of O
 
 template <int D>
 struct Cfg {
   static constexpr int kPanels = D / 64;                    // 128-byte swizzle panels per row
   static constexpr int kPanelBytes = 128 * 128;             // 128 rows x 128 B
   static constexpr int kTileBytes = kPanels * kPanelBytes;  // one 128 x D bf16 tile
-  static constexpr int kStages = (D == 128) ? 4 : 6;        // K/V ring slots
+  static constexpr int kHalfBytes = kPanelBytes / 2;        // 64 rows of one panel
+  static constexpr int kStages = (D == 128) ? 5 : 10;       // K/V ring slots
   static constexpr int kQOff = 0;
-  static constexpr int kKVOff = 2 * kTileBytes;
-  static constexpr int kRedOff = kKVOff + kStages * kTileBytes;  // row-max exchange [2][2][128] f32
-  static constexpr int kBarOff = kRedOff + 2 * 2 * 128 * 4;
-  static constexpr int kSmemBytes = kBarOff + 256 + 1024;   // + barriers + align slack
+  static constexpr int kKVOff = kTileBytes;
+  static constexpr int kRedOff = kKVOff + kStages * kTileBytes;  // m hand-off [2][128] + l/m [2][2][128]
+  static constexpr int kBarOff = kRedOff + 6 * 128 * 4;
+  static constexpr int kSmemBytes = kBarOff + 512 + 1024;   // + barriers + align slack
   // Default number (of every 8) of score-column pairs whose exp2 runs as a
-  // polynomial on the FMA pipe instead of MUFU (D=64 has half the MMA work
-  // per exponential of D=128).  Overridable per launch for measurement.
-  static constexpr int kEmuDefault = (D == 128) ? 2 : 4;
+  // polynomial on the FMA pipe instead of MUFU (D=64 has half the MMA work per
+  // exponential of D=128).  Overridable per launch for measurement (DMHA_EMU).
+  static constexpr int kEmuDefault = (D == 128) ? 1 : 3;
   static constexpr uint32_t kIdescQK = ptx::make_idesc(1, kBM, kBN, 0, 0);
   static constexpr uint32_t kIdescPV = ptx::make_idesc(1, kBM, D, 0, 1);  // V is MN-major
 };
@@ -90,14 +89,14 @@ struct Params {
   void* out;
   float* lse;
   int out_mode;
-  int n_mblk;
+  int n_pairs;  // CTA pairs along the query axis
   unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
 
 // Timeline trace (measurement hook): clock64 stamps for the first kTraceCtas
 // CTAs of head 0 and their first kTraceTiles KV tiles.  Events:
-//  0/2: softmax WG0/WG1 saw S full   1/3: WG0/WG1 arrive P ready
-//  4/5: MMA warp saw P0/P1 ready     6: MMA warp issued S1(j+1)
+//  0/2: softmax WG0/WG1 saw S(j)   1/3: WG0/WG1 arrive P(j) ready
+//  4: MMA saw P(j) ready   5: MMA issued PV(j)   6: MMA issued S(j)
 constexpr int kTraceCtas = 4, kTraceEvents = 7, kTraceTiles = 64;
 __device__ __forceinline__ void trace_stamp(const Params& p, int ev, int j) {
   if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < kTraceCtas && j < kTraceTiles)
@@ -113,7 +112,8 @@ __device__ __forceinline__ float2 exp2_mufu2(float2 x) {
 // n = round(x) via the 1.5*2^23 magic add, f = x - n in [-0.5, 0.5],
 // 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5, below the
 // 2^-9 bf16 rounding P gets anyway), exponent added as (n << 23).
-// x is clamped at -126 so -inf (masked) gives ~0 and the exponent cannot wrap.
+// x is clamped at -126 so the exponent cannot wrap (only used on unmasked
+// tiles, whose entries are finite).
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   const float2 magic = make_float2(12582912.f, 12582912.f);
   x.x = fmaxf(x.x, -126.f);
@@ -130,17 +130,17 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__uint_as_float(rx), __uint_as_float(ry));
 }
 
-// P = exp2(S*scale*log2e - m) for this thread's 64 score columns, packed to
-// bf16 and written to its 32 P columns in TMEM (16-column chunks, so the fp32
-// scores die as P is produced).  Returns the fp32 sum of the 64 P values.
+// P = exp2(S*scale*log2e - m) for one 128-column score row, packed to bf16 and
+// written over the first 64 TMEM columns of the S buffer (16-column chunks, so
+// the fp32 scores die as P is produced).  Returns the fp32 sum of P.
 // EMU of every 8 column pairs use exp2_poly2 (FMA pipe), the rest MUFU.
 template <int EMU>
-__device__ __forceinline__ float exp_tile(float (&s)[64], float sl2, float m_use, uint32_t tP) {
+__device__ __forceinline__ float exp_tile(float (&s)[128], float sl2, float m_use, uint32_t tP) {
   const float2 sc2 = make_float2(sl2, sl2);
   const float2 nm2 = make_float2(-m_use, -m_use);
   float2 sum_a = make_float2(0.f, 0.f), sum_b = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
+  for (int c = 0; c < 4; ++c) {
     uint32_t pk[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -159,10 +159,8 @@ __device__ __forceinline__ float exp_tile(float (&s)[64], float sl2, float m_use
   return (sum_a.x + sum_a.y) + (sum_b.x + sum_b.y);
 }
 
-// Named barrier over the 256 threads (two warpgroups) that share Q tile g.
-__device__ __forceinline__ void pair_sync(int g) {
-  asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
-}
+// Named barrier over the 256 softmax threads (both warpgroups).
+__device__ __forceinline__ void halves_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __device__ __forceinline__ int64_t pos_of(const PosMap& m, int64_t i) {
   return i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
@@ -185,16 +183,38 @@ __device__ __forceinline__ int64_t key_limit(const Params& p, int64_t qp) {
   return lim < p.Lk ? lim : p.Lk;
 }
 
-// KV tiles this CTA has to visit (a prefix of the key tiles).
-__device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
-  int64_t last = m0 + 2 * kBM - 1;
+// KV tiles the query rows [r0, r0 + n) need (a prefix of the key tiles).
+__device__ __forceinline__ int tiles_for_rows(const Params& p, int64_t r0, int64_t n) {
+  if (r0 >= p.Lq) return 0;
+  int64_t last = r0 + n - 1;
   if (last > p.Lq - 1) last = p.Lq - 1;
   const int64_t lim = key_limit(p, pos_of(p.qmap, last));
   return static_cast<int>((lim + kBN - 1) / kBN);
 }
 
-template <int D, int kEmu, bool kRegSplit>
-__global__ void __launch_bounds__(kThreads, 1)
+// The K/V load/consume sequence shared by producer and MMA issuer:
+//   K0, K1, K2, V0, K3, V1, K4, ..., V_{n-1}   (K_{t+3} right after V_t)
+// item i -> (is_v, tile).
+__device__ __forceinline__ void seq_item(int i, int n, bool& is_v, int& t) {
+  const int lead = n < kNB ? n : kNB;  // leading K loads
+  if (i < lead) {
+    is_v = false;
+    t = i;
+    return;
+  }
+  const int k = i - lead;  // pairs (V_t, K_{t+kNB}) while t + kNB < n, then V only
+  const int paired = n > kNB ? n - kNB : 0;
+  if (k < 2 * paired) {
+    is_v = (k & 1) == 0;
+    t = is_v ? (k >> 1) : (k >> 1) + kNB;
+  } else {
+    is_v = true;
+    t = paired + (k - 2 * paired);
+  }
+}
+
+template <int D, int kEmu>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const Params p) {
@@ -204,36 +224,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem + C::kQOff;
   uint8_t* sKV = smem + C::kKVOff;
-  float* red = reinterpret_cast<float*>(smem + C::kRedOff);  // [g][h][row]
+  float* red = reinterpret_cast<float*>(smem + C::kRedOff);  // [tile parity][half][row]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::kStages;
-  uint64_t* s_full = kv_empty + C::kStages;   // [2]
-  uint64_t* p_ready = s_full + 2;             // [2]
-  uint64_t* o_final = p_ready + 2;            // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
+  // Every barrier below is indexed so that its waiter can never be two phases
+  // behind (parity waits are only exact within one phase):
+  //  s_full[t%3]  S(t) written      — S(t+3) needs PV(t), i.e. P(t) consumed
+  //  p_ready[t%3] P(t) written      — P(t+3) needs S(t+3), issued after PV(t)
+  //  pv_done[t%2] PV(t) complete    — waited (for the rare O rescale) by tile
+  //               t+1's softmax, when PV(t-2) is known complete (S(t+1) was
+  //               issued after it) and PV(t+2) cannot have been issued
+  //  o_final      last PV complete  — one phase
+  uint64_t* s_full = kv_empty + C::kStages;  // [3]
+  uint64_t* p_ready = s_full + kNB;          // [3]
+  uint64_t* pv_done = p_ready + kNB;         // [2]
+  uint64_t* o_final = pv_done + 2;           // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int head = blockIdx.y;
-  // Causal: heaviest query blocks first.
-  const int mblk = p.causal ? (p.n_mblk - 1 - static_cast<int>(blockIdx.x))
-                            : static_cast<int>(blockIdx.x);
-  const int64_t m0 = static_cast<int64_t>(mblk) * (2 * kBM);
-  const int nkv = num_kv_tiles(p, m0);
+  const uint32_t crank = ptx::cluster_ctarank();
+  // Causal: heaviest query pairs first.
+  const int pair = p.causal ? (p.n_pairs - 1 - static_cast<int>(blockIdx.x >> 1))
+                            : static_cast<int>(blockIdx.x >> 1);
+  const int64_t m_pair = static_cast<int64_t>(pair) * (2 * kBM);
+  const int64_t m0 = m_pair + crank * kBM;
+  const int n_load = tiles_for_rows(p, m_pair, 2 * kBM);  // tiles the pair streams
+  const int n_own = tiles_for_rows(p, m0, kBM);           // tiles this CTA computes
+  const int n_items = 2 * n_load;
 
   if (warp == kProducerWarp && lane == 0) {
     ptx::mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&kv_empty[s], 2);  // released by both CTAs' MMA issuers
     }
-    for (int g = 0; g < 2; ++g) {
-      ptx::mbar_init(&s_full[g], 1);
-      ptx::mbar_init(&p_ready[g], 2 * kBM);  // both column halves of every row
-      ptx::mbar_init(&o_final[g], 1);
+    for (int b = 0; b < kNB; ++b) {
+      ptx::mbar_init(&s_full[b], 1);
+      ptx::mbar_init(&p_ready[b], kBM);  // the 128 threads of the tile's warpgroup
     }
+    ptx::mbar_init(&pv_done[0], 1);
+    ptx::mbar_init(&pv_done[1], 1);
+    ptx::mbar_init(o_final, 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
@@ -241,186 +276,174 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == kMmaWarp) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // peer barriers initialised before any multicast lands
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
-    if (kRegSplit) ptx::setmaxnreg_dec<kRegsCtl>();
-    if (lane == 0 && nkv > 0) {
-      ptx::mbar_arrive_expect_tx(q_full, 2 * C::kTileBytes);
-      for (int g = 0; g < 2; ++g)
+    if (lane == 0) {
+      if (n_own > 0) {
+        ptx::mbar_arrive_expect_tx(q_full, C::kTileBytes);
         for (int pn = 0; pn < C::kPanels; ++pn)
-          ptx::tma_load_3d(&tm_q, q_full, sQ + g * C::kTileBytes + pn * C::kPanelBytes, pn * 64,
-                           head, static_cast<int32_t>(m0 + g * kBM));
+          ptx::tma_load_3d(&tm_q, q_full, sQ + pn * C::kPanelBytes, pn * 64, head,
+                           static_cast<int32_t>(m0));
+      }
       int stage = 0;
       uint32_t phase = 0;
-      for (int j = 0; j < nkv; ++j) {
-        for (int which = 0; which < 2; ++which) {
-          ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
-          const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
-          for (int pn = 0; pn < C::kPanels; ++pn)
-            ptx::tma_load_3d(tm, &kv_full[stage], sKV + stage * C::kTileBytes + pn * C::kPanelBytes,
-                             pn * 64, head, j * kBN);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-        }
+      for (int i = 0; i < n_items; ++i) {
+        bool is_v;
+        int t;
+        seq_item(i, n_load, is_v, t);
+        ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
+        // This CTA loads rows [64*crank, 64*crank+64) of the tile into both CTAs.
+        const CUtensorMap* tm = is_v ? &tm_v : &tm_k;
+        for (int pn = 0; pn < C::kPanels; ++pn)
+          ptx::tma_load_3d_mc(tm, &kv_full[stage],
+                              sKV + stage * C::kTileBytes + pn * C::kPanelBytes +
+                                  crank * C::kHalfBytes,
+                              pn * 64, head, t * kBN + static_cast<int>(crank) * 64, 0x3);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+      // Drain: every slot's last fill released by both CTAs, so no remote
+      // arrive can target this CTA's shared memory after it exits.
+      for (int i = 0; i < C::kStages; ++i) {
+        ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (kRegSplit) ptx::setmaxnreg_dec<kRegsCtl>();
-    if (lane == 0 && nkv > 0) {
-      const uint32_t sq = ptx::smem_u32(sQ);
-      const uint32_t skv = ptx::smem_u32(sKV);
-      auto qk = [&](int g, int slot) {
-        const uint32_t a0 = sq + g * C::kTileBytes;
-        const uint32_t b0 = skv + slot * C::kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kPanelBytes + (kk & 3) * 32;
-          ptx::mma_bf16_ss(tmem + g * kBN, ptx::smem_desc_sw128(a0 + off, 16, 1024),
-                           ptx::smem_desc_sw128(b0 + off, 16, 1024), C::kIdescQK, kk > 0);
-        }
-      };
-      auto pv = [&](int g, int slot, bool acc) {
-        const uint32_t b0 = skv + slot * C::kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          ptx::mma_bf16_ts(tmem + 256 + g * 128, tmem + g * kBN + kk * 8,
-                           ptx::smem_desc_sw128(b0 + kk * 16 * 128, C::kPanelBytes, 1024),
-                           C::kIdescPV, (acc || kk > 0) ? 1u : 0u);
-        }
-      };
-      int stage = 0;
-      uint32_t phase = 0;
-      auto advance = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
-
-      ptx::mbar_wait(q_full, 0);
-      // j = 0
-      int slotK = stage;
-      ptx::mbar_wait(&kv_full[slotK], phase);
-      advance();
+    // The whole warp runs this loop (converged, warp-uniform operands); one
+    // elected lane issues each tcgen05 instruction.
+    // Descriptors are built once; per MMA only a compile-time offset (and the
+    // ring slot's offset) is added to the start-address field (bits [0,14),
+    // no carry: shared addresses are < 2^18).
+    const uint64_t dq = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 16, 1024);               // K-major
+    const uint64_t dk = ptx::smem_desc_sw128(ptx::smem_u32(sKV), 16, 1024);              // K-major
+    const uint64_t dv = ptx::smem_desc_sw128(ptx::smem_u32(sKV), C::kPanelBytes, 1024);  // MN-major
+    if (n_own > 0) ptx::mbar_wait(q_full, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < n_items; ++i) {
+      bool is_v;
+      int t;
+      seq_item(i, n_load, is_v, t);
+      ptx::mbar_wait(&kv_full[stage], phase);
       ptx::tc_fence_after();
-      qk(0, slotK);
-      ptx::mma_commit(&s_full[0]);
-      qk(1, slotK);
-      ptx::mma_commit(&s_full[1]);
-      ptx::mma_commit(&kv_empty[slotK]);
-      for (int j = 1; j <= nkv; ++j) {
-        const int slotV = stage;  // V_{j-1}
-        ptx::mbar_wait(&kv_full[slotV], phase);
-        advance();
-        const bool more = j < nkv;
-        int slotK2 = -1;
-        if (more) {
-          slotK2 = stage;  // K_j
-          ptx::mbar_wait(&kv_full[slotK2], phase);
-          advance();
-        }
-        const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
-        ptx::mbar_wait(&p_ready[0], ppar);
-        trace_stamp(p, 4, j - 1);
-        ptx::tc_fence_after();
-        pv(0, slotV, j > 1);
-        if (more) {
-          qk(0, slotK2);
-          ptx::mma_commit(&s_full[0]);
+      const uint64_t soff = static_cast<uint64_t>(stage * (C::kTileBytes >> 4));
+      if (t < n_own) {
+        const uint32_t sbuf = tmem + (t % kNB) * kBN;
+        if (!is_v) {
+          // S(t) = Q K_t^T into S buffer t%3 (after PV(t-3) read P(t-3) there)
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t off = ((kk >> 2) * C::kPanelBytes + (kk & 3) * 32) >> 4;
+            ptx::mma_bf16_ss_w(sbuf, dq + off, dk + soff + off, C::kIdescQK, kk > 0);
+          }
+          ptx::mma_commit_w(&s_full[t % kNB]);
+          if (lane == 0) trace_stamp(p, 6, t);
         } else {
-          ptx::mma_commit(&o_final[0]);
-        }
-        ptx::mbar_wait(&p_ready[1], ppar);
-        trace_stamp(p, 5, j - 1);
-        ptx::tc_fence_after();
-        pv(1, slotV, j > 1);
-        ptx::mma_commit(&kv_empty[slotV]);
-        if (more) {
-          qk(1, slotK2);
-          ptx::mma_commit(&s_full[1]);
-          trace_stamp(p, 6, j);
-          ptx::mma_commit(&kv_empty[slotK2]);
-        } else {
-          ptx::mma_commit(&o_final[1]);
+          // O += P(t) V_t, P(t) read from TMEM (S buffer t%3)
+          ptx::mbar_wait(&p_ready[t % kNB], static_cast<uint32_t>((t / kNB) & 1));
+          if (lane == 0) trace_stamp(p, 4, t);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk)
+            ptx::mma_bf16_ts_w(tmem + kOCol, sbuf + kk * 8, dv + soff + ((kk * 16 * 128) >> 4),
+                               C::kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
+          ptx::mma_commit_w(&pv_done[t & 1]);
+          if (t == n_own - 1) ptx::mma_commit_w(o_final);
+          if (lane == 0) trace_stamp(p, 5, t);
         }
       }
+      ptx::mma_commit_mc_w(&kv_empty[stage], 0x3);  // release the slot in both CTAs
+      if (++stage == C::kStages) { stage = 0; phase ^= 1; }
     }
     __syncwarp();
-  } else if (warp >= kSoftmaxWarps) {
-    if (kRegSplit) ptx::setmaxnreg_dec<kRegsCtl>();  // idle warps of the control warpgroup
-  } else {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ softmax
-    if (kRegSplit) ptx::setmaxnreg_inc<kRegsSoftmax>();
-    const int wg = warp >> 2;
-    const int g = wg >> 1;                    // Q tile of this warpgroup
-    const int h = wg & 1;                     // score-column half / output-column half
+    // Warpgroup w handles the KV tiles j = w (mod 2) — it always reads S
+    // buffer w — with one full 128-column score row per thread.  The only
+    // hand-off between the two warpgroups is the running max m: the warpgroup
+    // of tile j publishes m_j (per row) right after its row max, and the other
+    // warpgroup reads it before the exponentials of tile j+1.  Each keeps its
+    // own partial row sum l_w (relative to the m of its last tile); they are
+    // merged in the epilogue.  The two warpgroups' MUFU phases thus overlap
+    // instead of both waiting on a per-tile exchange.
+    const int w = warp >> 2;                  // tile parity this warpgroup owns
     const int quarter = warp & 3;             // TMEM lane quarter
     const int r = quarter * 32 + lane;        // row within the tile
-    const int64_t row = m0 + g * kBM + r;     // local query row
+    const int64_t row = m0 + r;               // local query row
     const bool row_ok = row < p.Lq;
     const int64_t qp = pos_of(p.qmap, row_ok ? row : p.Lq - 1);
     const int64_t klim = key_limit(p, qp);
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + g * kBN + h * 64;  // this half's 64 score columns
-    const uint32_t tP = tmem + lane_addr + g * kBN + h * 32;  // this half's 32 P columns
-    const uint32_t tO = tmem + lane_addr + 256 + g * 128;
-    float* red_mine = red + (g * 2 + h) * kBM + r;
-    const float* red_other = red + (g * 2 + (h ^ 1)) * kBM + r;
+    const uint32_t tO = tmem + lane_addr + kOCol;
     const float sl2 = p.scale_log2;
-    const bool leader = (threadIdx.x % 256) == 0;  // one stamp per Q tile
+    const bool leader = (threadIdx.x % 128) == 0;
+    float* mrow = red;  // [tile parity][row]: m_j published by tile j's warpgroup
 
-    float m_run = -INFINITY;  // running max, log2 units (scaled); equal in both halves
-    float l_run = 0.f;        // this half's share of the row sum
-    for (int j = 0; j < nkv; ++j) {
-      ptx::mbar_wait(&s_full[g], static_cast<uint32_t>(j & 1));
-      if (leader) trace_stamp(p, 2 * g, j);
+    float m_prev = -INFINITY;  // m of this warpgroup's last tile (log2 units, scaled)
+    float l_run = 0.f;         // this warpgroup's partial row sum, relative to m_prev
+    for (int j = w; j < n_own; j += 2) {
+      const uint32_t sbuf = tmem + lane_addr + (j % kNB) * kBN;  // S(j), then P(j)
+      ptx::mbar_wait(&s_full[j % kNB], static_cast<uint32_t>((j / kNB) & 1));
+      if (leader) trace_stamp(p, 2 * w, j);
       ptx::tc_fence_after();
-      float s[64];
-      ptx::tmem_ld32(tS, *reinterpret_cast<float(*)[32]>(&s[0]));
-      ptx::tmem_ld32(tS + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        ptx::tmem_ld32(sbuf + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
       ptx::tmem_wait_ld();
 
-      const int64_t nv64 = klim - static_cast<int64_t>(j) * kBN - h * 64;
-      const int nvalid = nv64 < 0 ? 0 : (nv64 > 64 ? 64 : static_cast<int>(nv64));
-      // Warp-uniform in both halves of a row: masked iff any row of the Q tile
-      // has fewer than all 128 keys of the tile visible.
-      const bool masked = !__all_sync(0xffffffffu, klim - static_cast<int64_t>(j) * kBN >= kBN);
+      const int64_t nv64 = klim - static_cast<int64_t>(j) * kBN;
+      const int nvalid = nv64 < 0 ? 0 : (nv64 > kBN ? kBN : static_cast<int>(nv64));
+      const bool masked = !__all_sync(0xffffffffu, nvalid >= kBN);
       if (masked) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
+        for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
       float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
 #pragma unroll
-      for (int c = 4; c < 64; c += 4) {
+      for (int c = 4; c < 128; c += 4) {
         mx0 = fmaxf(mx0, s[c]);
         mx1 = fmaxf(mx1, s[c + 1]);
         mx2 = fmaxf(mx2, s[c + 2]);
         mx3 = fmaxf(mx3, s[c + 3]);
       }
-      const float pmax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-      *red_mine = pmax;
-      pair_sync(g);  // the other half reads this slot before tile j+1 can be
-                     // written: S_g(j+1) needs both halves' P_g(j) first.
-      const float mt = fmaxf(pmax, *red_other) * sl2;
-      const bool need = mt > m_run + kRescaleThreshold;
-      const bool warp_rescale = __any_sync(0xffffffffu, need);  // same in both halves
-      float alpha = 1.f;
-      if (warp_rescale) {
-        const float m_new = fmaxf(m_run, mt);
-        alpha = (m_new == -INFINITY) ? 1.f : ptx::ex2_approx(m_run - m_new);
-        l_run *= alpha;
-        m_run = m_new;
+      const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      // m_{j-1} from the other warpgroup (tile j-1), published on barrier 2+(1-w).
+      float m_in = -INFINITY;
+      if (j > 0) {
+        asm volatile("bar.sync %0, 256;" ::"r"(2 + (w ^ 1)) : "memory");
+        m_in = mrow[((j - 1) & 1) * kBM + r];
       }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      const bool need = mt > m_in + kRescaleThreshold;
+      const float m_cur = __any_sync(0xffffffffu, need) ? fmaxf(m_in, mt) : m_in;
+      if (j + 1 < n_own) {  // hand m_j to the warpgroup of tile j+1
+        mrow[(j & 1) * kBM + r] = m_cur;
+        asm volatile("bar.arrive %0, 256;" ::"r"(2 + w) : "memory");
+      }
+      // This warpgroup's partial sum was accumulated relative to m_prev.
+      if (m_cur != m_prev) {
+        l_run *= (m_prev == -INFINITY) ? 0.f : ptx::ex2_approx(m_prev - m_cur);
+      }
+      const float m_use = (m_cur == -INFINITY) ? 0.f : m_cur;
       // Unmasked tiles send kEmu of every 8 column pairs to the FMA-pipe
       // polynomial; masked tiles (-inf entries, must give exactly 0) use MUFU only.
       if (masked)
-        l_run += exp_tile<0>(s, sl2, m_use, tP);
+        l_run += exp_tile<0>(s, sl2, m_use, sbuf);
       else
-        l_run += exp_tile<kEmu>(s, sl2, m_use, tP);
-      // O_g holds PV_g(j-1) (complete: covered by the S_g(j) commit) and PV_g(j)
-      // is not issued before p_ready, so O can be rescaled in place here.
-      if (warp_rescale && j > 0 && h == 0) {
+        l_run += exp_tile<kEmu>(s, sl2, m_use, sbuf);
+      // O holds PV(0..j-2) and possibly PV(j-1) in flight; PV(j) waits for
+      // p_ready.  If this warp's max moved, rescale its O rows after PV(j-1)
+      // completes (at most one pv_done phase can be pending here).
+      if (j > 0 && __any_sync(0xffffffffu, m_cur != m_in)) {
+        const float alpha = (m_in == -INFINITY || m_cur == m_in) ? 1.f : ptx::ex2_approx(m_in - m_cur);
+        ptx::mbar_wait(&pv_done[(j - 1) & 1], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+        ptx::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           float o[32];
@@ -431,31 +454,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_st32(tO + c * 32, o);
         }
       }
+      m_prev = m_cur;
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      if (leader) trace_stamp(p, 2 * g + 1, j);
-      ptx::mbar_arrive(&p_ready[g]);
+      if (leader) trace_stamp(p, 2 * w + 1, j);
+      ptx::mbar_arrive(&p_ready[j % kNB]);
     }
-    if (nkv > 0) {
-      ptx::mbar_wait(&o_final[g], 0);
+    if (n_own > 0) {
+      ptx::mbar_wait(o_final, 0);
       ptx::tc_fence_after();
     }
     // ---------------------------------------------------------- epilogue
-    // Row sum = both halves' shares (same m_run); each half writes D/2 columns.
-    *red_mine = l_run;
-    pair_sync(g);
-    const float l_tot = l_run + *red_other;
+    // Merge the two partial sums at the final max; each warpgroup then writes
+    // D/2 output columns of every row.
+    float* lx = red + 2 * kBM;  // [w][row] (l, m) pairs
+    lx[(w * 2 + 0) * kBM + r] = l_run;
+    lx[(w * 2 + 1) * kBM + r] = m_prev;
+    halves_sync();
+    const float l_o = lx[((w ^ 1) * 2 + 0) * kBM + r];
+    const float m_o = lx[((w ^ 1) * 2 + 1) * kBM + r];
+    const float m_fin = fmaxf(m_prev, m_o);
+    float l_tot = 0.f;
+    if (m_fin != -INFINITY) {
+      l_tot = (m_prev == -INFINITY ? 0.f : l_run * ptx::ex2_approx(m_prev - m_fin)) +
+              (m_o == -INFINITY ? 0.f : l_o * ptx::ex2_approx(m_o - m_fin));
+    }
     const bool empty = !(l_tot > 0.f);
     const float inv_l = empty ? 0.f : 1.f / l_tot;
-    if (row_ok && h == 0)
+    if (row_ok && w == 0)
       p.lse[static_cast<int64_t>(head) * p.Lq + row] =
-          empty ? -INFINITY : (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
-    const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D) + h * (D / 2);
+          empty ? -INFINITY : (m_fin + __log2f(l_tot)) * 0.69314718055994530942f;
+    const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D) + w * (D / 2);
 #pragma unroll
     for (int c = 0; c < D / 64; ++c) {
       float o[32];
-      if (nkv > 0) {
-        ptx::tmem_ld32(tO + h * (D / 2) + c * 32, o);
+      if (n_own > 0) {
+        ptx::tmem_ld32(tO + w * (D / 2) + c * 32, o);
         ptx::tmem_wait_ld();
       } else {
 #pragma unroll
@@ -473,14 +507,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                 c * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            uint32_t w[4];
+            uint32_t wd[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               __nv_bfloat162 b = __floats2bfloat162_rn(o[8 * e + 2 * t] * inv_l,
                                                        o[8 * e + 2 * t + 1] * inv_l);
-              w[t] = *reinterpret_cast<uint32_t*>(&b);
+              wd[t] = *reinterpret_cast<uint32_t*>(&b);
             }
-            dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[e] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
           }
         }
       }
@@ -492,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
+  ptx::cluster_sync();  // the peer may still multicast into / arrive on this CTA until here
 }
 
 // ---------------------------------------------------------------- host side
@@ -514,16 +549,16 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// [L, H, D] bf16 viewed as a 3-D tensor (D, H, L); box (64, 1, 128), 128B swizzle.
-bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
+// [L, H, D] bf16 viewed as a 3-D tensor (D, H, L); box (64, 1, box_rows), 128B swizzle.
+bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D, int box_rows) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
-  // A zero-length block is never loaded (nkv = 0) but the map must be valid.
+  // A zero-length block is never loaded (no KV tiles) but the map must be valid.
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(H),
                         static_cast<cuuint64_t>(L > 0 ? L : 1)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2,
                            static_cast<cuuint64_t>(D) * H * 2};
-  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -532,45 +567,38 @@ bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
   return r == CUDA_SUCCESS;
 }
 
-// Kernel variant (measurement knob): DMHA_EMU=<pairs of 8 on the FMA pipe>,
-// DMHA_REGSPLIT=0/1.  Defaults: Cfg<D>::kEmuDefault, register split on.
-struct Variant {
-  int emu;
-  bool regsplit;
-};
-
+// Kernel variant (measurement knob): DMHA_EMU=<pairs of 8 on the FMA pipe>.
 template <int D>
-Variant variant() {
-  static Variant v = [] {
-    Variant x{Cfg<D>::kEmuDefault, true};
-    if (const char* e = std::getenv("DMHA_EMU")) x.emu = std::atoi(e);
-    if (const char* r = std::getenv("DMHA_REGSPLIT")) x.regsplit = std::atoi(r) != 0;
+int emu_variant() {
+  static int v = [] {
+    int x = Cfg<D>::kEmuDefault;
+    if (const char* e = std::getenv("DMHA_EMU")) x = std::atoi(e);
     return x;
   }();
   return v;
 }
 
-template <int D, int E, bool R>
+template <int D, int E>
 cudaError_t launch_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const Params& p, dim3 grid, cudaStream_t stream) {
   using C = Cfg<D>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, R>,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  attn_fwd_sm100_kernel<D, E, R><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  attn_fwd_sm100_kernel<D, E><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
 template <int D>
 cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   CUtensorMap tq, tk, tv;
-  if (!make_map(&tq, a.q, a.Lq, a.H, D) || !make_map(&tk, a.k, a.Lk, a.H, D) ||
-      !make_map(&tv, a.v, a.Lk, a.H, D))
+  if (!make_map(&tq, a.q, a.Lq, a.H, D, kBM) || !make_map(&tk, a.k, a.Lk, a.H, D, kBN / 2) ||
+      !make_map(&tv, a.v, a.Lk, a.H, D, kBN / 2))
     return cudaErrorInvalidValue;
   Params p;
   p.Lq = a.Lq;
@@ -583,18 +611,16 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   p.out = a.out;
   p.lse = a.lse;
   p.out_mode = a.out_mode;
-  p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
+  p.n_pairs = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.trace = g_trace;
-  dim3 grid(p.n_mblk, a.H);
-  const Variant v = variant<D>();
-  if (!v.regsplit) return launch_v<D, Cfg<D>::kEmuDefault, false>(tq, tk, tv, p, grid, stream);
-  switch (v.emu) {
-    case 0: return launch_v<D, 0, true>(tq, tk, tv, p, grid, stream);
-    case 1: return launch_v<D, 1, true>(tq, tk, tv, p, grid, stream);
-    case 2: return launch_v<D, 2, true>(tq, tk, tv, p, grid, stream);
-    case 3: return launch_v<D, 3, true>(tq, tk, tv, p, grid, stream);
-    case 4: return launch_v<D, 4, true>(tq, tk, tv, p, grid, stream);
-    default: return launch_v<D, Cfg<D>::kEmuDefault, true>(tq, tk, tv, p, grid, stream);
+  dim3 grid(2 * p.n_pairs, a.H);
+  switch (emu_variant<D>()) {
+    case 0: return launch_v<D, 0>(tq, tk, tv, p, grid, stream);
+    case 1: return launch_v<D, 1>(tq, tk, tv, p, grid, stream);
+    case 2: return launch_v<D, 2>(tq, tk, tv, p, grid, stream);
+    case 3: return launch_v<D, 3>(tq, tk, tv, p, grid, stream);
+    case 4: return launch_v<D, 4>(tq, tk, tv, p, grid, stream);
+    default: return launch_v<D, Cfg<D>::kEmuDefault>(tq, tk, tv, p, grid, stream);
   }
 }
 

@@ -21,7 +21,7 @@ dmha.debug_set_trace(None)
 t = buf.view(4, 7, 64).cpu().numpy().astype(np.int64)
 for c in range(2):
     tc = t[c] - t[c][0][0]
-    print(f"CTA {c}: event rows (cycles rel. to WG0 first S): 0=S0 1=P0 2=S1 3=P1 4=mmaP0 5=mmaP1 6=mmaS1next")
+    print(f"CTA {c}: rows = tile j; cols = 0:WG0 saw S 1:WG0 P 2:WG1 saw S 3:WG1 P 4:mma saw P 5:mma PV issued 6:mma S issued")
     for j in range(8, 16):
         print(j, " ".join(f"{tc[e][j]:8d}" for e in range(7)))
     # steady-state stats over tiles 8..60
@@ -29,6 +29,6 @@ for c in range(2):
     per = np.diff(tc[0][8:60]).mean()
     sm0 = np.mean([tc[1][j] - tc[0][j] for j in js]); sm1 = np.mean([tc[3][j] - tc[2][j] for j in js])
     w0 = np.mean([tc[0][j + 1] - tc[1][j] for j in js]); w1 = np.mean([tc[2][j + 1] - tc[3][j] for j in js])
-    lat0 = np.mean([tc[4][j] - tc[1][j] for j in js])
-    print(f"  period/tile {per:.0f}  softmax0 {sm0:.0f}  softmax1 {sm1:.0f}  wait-S0 {w0:.0f}  wait-S1 {w1:.0f}  P0->mma-sees {lat0:.0f}")
+    lat0 = np.mean([tc[4][j] - max(tc[1][j], tc[3][j]) for j in js])
+    print(f"  period/tile {per:.0f}  softmax WG0 {sm0:.0f}  WG1 {sm1:.0f}  wait-S WG0 {w0:.0f}  WG1 {w1:.0f}  P->mma-sees {lat0:.0f}")
 dmha.finalize()
