@@ -175,7 +175,7 @@ int dmha_attention_local(const void *q, const void *k, const void *v, void *out,
 int dmha_lse_combine(float *o_acc, float *lse_acc, const float *o_part, const float *lse_part,
                      void *out, float *lse_out, int64_t Lq, int D, int H, int final_step);
 
-/* Measurement hook: dev_buf (device, >= 4*7*64 uint64, or NULL to disable)
+/* Measurement hook: dev_buf (device, >= 4*9*64 uint64, or NULL to disable)
  * receives clock64 timeline stamps of the bf16 attention kernel (first 4 CTAs
  * of head 0, first 64 KV tiles; events documented in attn_fwd_sm100.cu). */
 int dmha_debug_set_trace(void *dev_buf);

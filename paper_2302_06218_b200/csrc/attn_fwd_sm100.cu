@@ -43,6 +43,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "kernels.h"
 #include "ptx_sm100.cuh"
@@ -55,29 +56,41 @@ constexpr int kBM = 128;          // query rows per CTA (MMA M)
 constexpr int kBN = 128;          // keys per tile (MMA N of QK^T, K of PV)
 constexpr int kThreads = 384;     // 12 warps
 constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
+constexpr int kMmaWarp = 9;       // TMEM allocator; MMA issuer (pair path: S = QK^T only)
+constexpr int kPvWarp = 10;       // pair path: issues PV MMAs
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
 constexpr int kNB = 3;            // S buffers in TMEM (S(t+3) reuses buffer t%3 after PV(t))
 constexpr int kOCol = kNB * kBN;  // first TMEM column of O
 
-template <int D>
+// K2 = true: CTA-pair MMA (tcgen05 cta_group::2, M = 256).  Each CTA holds
+// its own 128 query rows and HALF of every K/V tile (64 keys of K, D/2 columns
+// of V), so L2->SMEM traffic is one K/V tile per 256 query rows and the pair
+// leader issues one MMA per 256 rows.  K2 = false: each CTA issues its own
+// M = 128 MMAs; the pair still shares K/V tiles by TMA multicast (each CTA
+// loads half and multicasts it into both).
+template <int D, bool K2>
 struct Cfg {
   static constexpr int kPanels = D / 64;                    // 128-byte swizzle panels per row
   static constexpr int kPanelBytes = 128 * 128;             // 128 rows x 128 B
   static constexpr int kTileBytes = kPanels * kPanelBytes;  // one 128 x D bf16 tile
   static constexpr int kHalfBytes = kPanelBytes / 2;        // 64 rows of one panel
-  static constexpr int kStages = (D == 128) ? 5 : 10;       // K/V ring slots
+  static constexpr int kQBytes = kTileBytes;                // this CTA's query tile
+  static constexpr int kSlotBytes = K2 ? kTileBytes / 2 : kTileBytes;  // one K/V ring slot
+  static constexpr int kKPanelStride = K2 ? kHalfBytes : kPanelBytes;   // K panel stride in a slot
+  static constexpr int kStages = K2 ? 11 : ((D == 128) ? 5 : 10);       // K/V ring slots
   static constexpr int kQOff = 0;
-  static constexpr int kKVOff = kTileBytes;
-  static constexpr int kRedOff = kKVOff + kStages * kTileBytes;  // m hand-off [2][128] + l/m [2][2][128]
+  static constexpr int kKVOff = kQBytes;
+  static constexpr int kRedOff = kKVOff + kStages * kSlotBytes;  // m hand-off [2][128] + l/m [2][2][128]
   static constexpr int kBarOff = kRedOff + 6 * 128 * 4;
   static constexpr int kSmemBytes = kBarOff + 512 + 1024;   // + barriers + align slack
   // Default number (of every 8) of score-column pairs whose exp2 runs as a
   // polynomial on the FMA pipe instead of MUFU (D=64 has half the MMA work per
   // exponential of D=128).  Overridable per launch for measurement (DMHA_EMU).
-  static constexpr int kEmuDefault = (D == 128) ? 1 : 3;
-  static constexpr uint32_t kIdescQK = ptx::make_idesc(1, kBM, kBN, 0, 0);
-  static constexpr uint32_t kIdescPV = ptx::make_idesc(1, kBM, D, 0, 1);  // V is MN-major
+  static constexpr int kEmuDefault = 0;  // measured best on B200 for both D
+  static constexpr uint32_t kM = K2 ? 256 : kBM;
+  static constexpr uint32_t kIdescQK = ptx::make_idesc(1, kM, kBN, 0, 0);
+  static constexpr uint32_t kIdescPV = ptx::make_idesc(1, kM, D, 0, 1);  // V is MN-major
+  static_assert(!K2 || D == 128, "the CTA-pair path splits V by 64-column panels (D = 128)");
 };
 
 struct Params {
@@ -97,7 +110,8 @@ struct Params {
 // CTAs of head 0 and their first kTraceTiles KV tiles.  Events:
 //  0/2: softmax WG0/WG1 saw S(j)   1/3: WG0/WG1 arrive P(j) ready
 //  4: MMA saw P(j) ready   5: MMA issued PV(j)   6: MMA issued S(j)
-constexpr int kTraceCtas = 4, kTraceEvents = 7, kTraceTiles = 64;
+//  7: MMA saw V_j landed    8: producer issued the V_j load
+constexpr int kTraceCtas = 4, kTraceEvents = 9, kTraceTiles = 64;
 __device__ __forceinline__ void trace_stamp(const Params& p, int ev, int j) {
   if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < kTraceCtas && j < kTraceTiles)
     p.trace[(blockIdx.x * kTraceEvents + ev) * kTraceTiles + j] = clock64();
@@ -213,12 +227,12 @@ __device__ __forceinline__ void seq_item(int i, int n, bool& is_v, int& t) {
   }
 }
 
-template <int D, int kEmu>
+template <int D, int kEmu, bool K2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const Params p) {
-  using C = Cfg<D>;
+  using C = Cfg<D, K2>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -233,14 +247,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // behind (parity waits are only exact within one phase):
   //  s_full[t%3]  S(t) written      — S(t+3) needs PV(t), i.e. P(t) consumed
   //  p_ready[t%3] P(t) written      — P(t+3) needs S(t+3), issued after PV(t)
-  //  pv_done[t%2] PV(t) complete    — waited (for the rare O rescale) by tile
-  //               t+1's softmax, when PV(t-2) is known complete (S(t+1) was
-  //               issued after it) and PV(t+2) cannot have been issued
+  //  pv_done[..]  PV(t) complete    — per-CTA path: pv_done[t%2], waited (for
+  //               the rare O rescale) by tile t+1's softmax, when PV(t-2) is
+  //               known complete (S(t+1) was issued after it) and PV(t+2)
+  //               cannot have been issued.  Pair path: pv_done[t%3], also
+  //               waited by the S issuer before S(t+3) reuses buffer t%3.
   //  o_final      last PV complete  — one phase
   uint64_t* s_full = kv_empty + C::kStages;  // [3]
   uint64_t* p_ready = s_full + kNB;          // [3]
-  uint64_t* pv_done = p_ready + kNB;         // [2]
-  uint64_t* o_final = pv_done + 2;           // [1]
+  uint64_t* pv_done = p_ready + kNB;         // [3]
+  uint64_t* o_final = pv_done + 3;           // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -253,28 +269,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int64_t m_pair = static_cast<int64_t>(pair) * (2 * kBM);
   const int64_t m0 = m_pair + crank * kBM;
   const int n_load = tiles_for_rows(p, m_pair, 2 * kBM);  // tiles the pair streams
-  const int n_own = tiles_for_rows(p, m0, kBM);           // tiles this CTA computes
+  // With the pair MMA both CTAs step through the pair's tiles together (rows a
+  // tile does not reach are masked); otherwise a CTA stops at its own last tile.
+  const int n_own = K2 ? n_load : tiles_for_rows(p, m0, kBM);
   const int n_items = 2 * n_load;
 
   if (warp == kProducerWarp && lane == 0) {
     ptx::mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 2);  // released by both CTAs' MMA issuers
+      ptx::mbar_init(&kv_empty[s], K2 ? 1 : 2);  // released by the MMA issuer(s) of the pair
     }
     for (int b = 0; b < kNB; ++b) {
       ptx::mbar_init(&s_full[b], 1);
-      ptx::mbar_init(&p_ready[b], kBM);  // the 128 threads of the tile's warpgroup
+      // K2: one arrive per softmax warp of both CTAs (on the leader's barrier);
+      // else the 128 threads of the tile's warpgroup.
+      ptx::mbar_init(&p_ready[b], K2 ? 8 : kBM);
     }
-    ptx::mbar_init(&pv_done[0], 1);
-    ptx::mbar_init(&pv_done[1], 1);
+    for (int b = 0; b < 3; ++b) ptx::mbar_init(&pv_done[b], 1);
     ptx::mbar_init(o_final, 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
   }
-  if (warp == kMmaWarp) ptx::tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarp) {
+    if (K2)
+      ptx::tmem_alloc_2cta<512>(tmem_slot);
+    else
+      ptx::tmem_alloc<512>(tmem_slot);
+  }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // peer barriers initialised before any multicast lands
   ptx::tc_fence_after();
@@ -282,9 +306,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    if (lane == 0 && K2) {
+      // Pair MMA: each CTA loads its own Q rows and its half of every K/V tile
+      // into its own shared memory; completion is counted on the leader's
+      // barriers (the leader alone waits on them and issues the MMAs).
+      const uint32_t q_full_l = ptx::mapa_cluster(q_full, 0);
+      if (n_load > 0) {
+        if (crank == 0) ptx::mbar_arrive_expect_tx(q_full, 2 * C::kQBytes);
+        for (int pn = 0; pn < C::kPanels; ++pn)
+          ptx::tma_load_3d_2sm(&tm_q, q_full_l, sQ + pn * C::kPanelBytes, pn * 64, head,
+                               static_cast<int32_t>(m0));
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < n_items; ++i) {
+        bool is_v;
+        int t;
+        seq_item(i, n_load, is_v, t);
+        ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+        if (is_v) trace_stamp(p, 8, t);
+        if (crank == 0) ptx::mbar_arrive_expect_tx(&kv_full[stage], 2 * C::kSlotBytes);
+        const uint32_t full_l = ptx::mapa_cluster(&kv_full[stage], 0);
+        uint8_t* slot = sKV + stage * C::kSlotBytes;
+        if (!is_v) {  // K: keys [64*crank, 64*crank+64) of the tile, all D columns
+          for (int pn = 0; pn < C::kPanels; ++pn)
+            ptx::tma_load_3d_2sm(&tm_k, full_l, slot + pn * C::kKPanelStride, pn * 64, head,
+                                 t * kBN + static_cast<int>(crank) * 64);
+        } else {      // V: all 128 keys of the tile, columns [64*crank, 64*crank+64)
+          ptx::tma_load_3d_2sm(&tm_v, full_l, slot, static_cast<int>(crank) * 64, head, t * kBN);
+        }
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+      for (int i = 0; i < C::kStages; ++i) {  // drain (see below)
+        ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+    } else if (lane == 0) {
       if (n_own > 0) {
-        ptx::mbar_arrive_expect_tx(q_full, C::kTileBytes);
+        ptx::mbar_arrive_expect_tx(q_full, C::kQBytes);
         for (int pn = 0; pn < C::kPanels; ++pn)
           ptx::tma_load_3d(&tm_q, q_full, sQ + pn * C::kPanelBytes, pn * 64, head,
                            static_cast<int32_t>(m0));
@@ -296,17 +355,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int t;
         seq_item(i, n_load, is_v, t);
         ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+        if (is_v) trace_stamp(p, 8, t);
         ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
         // This CTA loads rows [64*crank, 64*crank+64) of the tile into both CTAs.
         const CUtensorMap* tm = is_v ? &tm_v : &tm_k;
         for (int pn = 0; pn < C::kPanels; ++pn)
           ptx::tma_load_3d_mc(tm, &kv_full[stage],
-                              sKV + stage * C::kTileBytes + pn * C::kPanelBytes +
+                              sKV + stage * C::kSlotBytes + pn * C::kPanelBytes +
                                   crank * C::kHalfBytes,
                               pn * 64, head, t * kBN + static_cast<int>(crank) * 64, 0x3);
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
-      // Drain: every slot's last fill released by both CTAs, so no remote
+      // Drain: every slot's last fill released by the pair, so no remote
       // arrive can target this CTA's shared memory after it exits.
       for (int i = 0; i < C::kStages; ++i) {
         ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
@@ -317,48 +377,120 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs this loop (converged, warp-uniform operands); one
     // elected lane issues each tcgen05 instruction.
-    // Descriptors are built once; per MMA only a compile-time offset (and the
-    // ring slot's offset) is added to the start-address field (bits [0,14),
-    // no carry: shared addresses are < 2^18).
-    const uint64_t dq = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 16, 1024);               // K-major
-    const uint64_t dk = ptx::smem_desc_sw128(ptx::smem_u32(sKV), 16, 1024);              // K-major
-    const uint64_t dv = ptx::smem_desc_sw128(ptx::smem_u32(sKV), C::kPanelBytes, 1024);  // MN-major
-    if (n_own > 0) ptx::mbar_wait(q_full, 0);
+    // Operands are kept warp-uniform and 32-bit: descriptors are passed as
+    // their low word (start address >> 4 in [0,14), LBO >> 4 in [16,30)) plus
+    // a constant high word (SBO = 1024 B, version 1, SWIZZLE_128B).  The start
+    // field holds the shared address modulo 2^18 (a CTA of a cluster can sit
+    // above 256 KB in the shared window), hence the 14-bit mask.
+    constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+    constexpr uint32_t kLboK = (16u >> 4) << 16;                        // K-major: unused
+    constexpr uint32_t kLboV = (uint32_t(C::kPanelBytes) >> 4) << 16;   // MN-major V: panel stride
+    const uint32_t sal = ptx::smem_u32(smem);
+    const uint32_t q_lo = (((sal + C::kQOff) >> 4) & 0x3FFFu) | kLboK;
+    const uint32_t k_lo = (((sal + C::kKVOff) >> 4) & 0x3FFFu) | kLboK;
+    const uint32_t v_lo = (((sal + C::kKVOff) >> 4) & 0x3FFFu) | kLboV;
+    if (!K2) {
+      if (n_own > 0) ptx::mbar_wait(q_full, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < n_items; ++i) {
+        bool is_v;
+        int t;
+        seq_item(i, n_load, is_v, t);
+        ptx::mbar_wait(&kv_full[stage], phase);
+        if (is_v && lane == 0) trace_stamp(p, 7, t);
+        ptx::tc_fence_after();
+        const uint32_t soff = static_cast<uint32_t>(stage) * (C::kSlotBytes >> 4);
+        if (t < n_own) {
+          const uint32_t sbuf = tmem + static_cast<uint32_t>(t % kNB) * kBN;  // S(t) columns
+          if (!is_v) {
+            // S(t) = Q K_t^T into S buffer t%3 (after PV(t-3) read P(t-3) there)
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t aoff = ((kk >> 2) * C::kPanelBytes + (kk & 3) * 32) >> 4;
+              const uint32_t boff = ((kk >> 2) * C::kKPanelStride + (kk & 3) * 32) >> 4;
+              ptx::mma_bf16_ss_lo(sbuf, q_lo + aoff, k_lo + soff + boff, kDescHi, C::kIdescQK, kk > 0);
+            }
+            ptx::mma_commit_w(&s_full[t % kNB]);
+            if (lane == 0) trace_stamp(p, 6, t);
+          } else {
+            // O += P(t) V_t, P(t) read from TMEM (S buffer t%3)
+            ptx::mbar_wait(&p_ready[t % kNB], static_cast<uint32_t>((t / kNB) & 1));
+            if (lane == 0) trace_stamp(p, 4, t);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < kBN / 16; ++kk)
+              ptx::mma_bf16_ts_lo(tmem + kOCol, sbuf + kk * 8, v_lo + soff + ((kk * 16 * 128) >> 4),
+                                  kDescHi, C::kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_commit_w(&pv_done[t & 1]);
+            if (t == n_own - 1) ptx::mma_commit_w(o_final);
+            if (lane == 0) trace_stamp(p, 5, t);
+          }
+        }
+        ptx::mma_commit_mc_w(&kv_empty[stage], 0x3);  // release the slot in both CTAs
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+    } else if (crank == 0) {
+      // Pair path, S issuer (leader only): S(t) = Q K_t^T for the whole pair.
+      // S(t) reuses buffer t%3 once PV(t-3) — issued by the PV warp — is
+      // complete; the two issuers keep the tensor core's short queue fed.
+      if (n_own > 0) ptx::mbar_wait(q_full, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < n_items; ++i) {
+        bool is_v;
+        int t;
+        seq_item(i, n_load, is_v, t);
+        if (!is_v) {
+          ptx::mbar_wait(&kv_full[stage], phase);
+          if (t >= kNB) ptx::mbar_wait(&pv_done[t % kNB], static_cast<uint32_t>(((t - kNB) / kNB) & 1));
+          ptx::tc_fence_after();
+          const uint32_t soff = static_cast<uint32_t>(stage) * (C::kSlotBytes >> 4);
+          const uint32_t sbuf = tmem + static_cast<uint32_t>(t % kNB) * kBN;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t aoff = ((kk >> 2) * C::kPanelBytes + (kk & 3) * 32) >> 4;
+            const uint32_t boff = ((kk >> 2) * C::kKPanelStride + (kk & 3) * 32) >> 4;
+            ptx::mma2_bf16_ss_lo(sbuf, q_lo + aoff, k_lo + soff + boff, kDescHi, C::kIdescQK, kk > 0);
+          }
+          ptx::mma2_commit_mc_w(&s_full[t % kNB], 0x3);
+          ptx::mma2_commit_mc_w(&kv_empty[stage], 0x3);
+          if (lane == 0) trace_stamp(p, 6, t);
+        }
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (K2 && warp == kPvWarp && crank == 0) {
+    // ------------------------------------------------------------ PV issuer
+    // Pair path (leader only): O += P(t) V_t once P(t) of both CTAs is ready.
+    const uint32_t sal = ptx::smem_u32(smem);
+    constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+    constexpr uint32_t kLboV = (uint32_t(C::kPanelBytes) >> 4) << 16;
+    const uint32_t v_lo = (((sal + C::kKVOff) >> 4) & 0x3FFFu) | kLboV;
     int stage = 0;
     uint32_t phase = 0;
     for (int i = 0; i < n_items; ++i) {
       bool is_v;
       int t;
       seq_item(i, n_load, is_v, t);
-      ptx::mbar_wait(&kv_full[stage], phase);
-      ptx::tc_fence_after();
-      const uint64_t soff = static_cast<uint64_t>(stage * (C::kTileBytes >> 4));
-      if (t < n_own) {
-        const uint32_t sbuf = tmem + (t % kNB) * kBN;
-        if (!is_v) {
-          // S(t) = Q K_t^T into S buffer t%3 (after PV(t-3) read P(t-3) there)
+      if (is_v) {
+        ptx::mbar_wait(&kv_full[stage], phase);
+        if (lane == 0) trace_stamp(p, 7, t);
+        ptx::mbar_wait(&p_ready[t % kNB], static_cast<uint32_t>((t / kNB) & 1));
+        if (lane == 0) trace_stamp(p, 4, t);
+        ptx::tc_fence_after();
+        const uint32_t soff = static_cast<uint32_t>(stage) * (C::kSlotBytes >> 4);
+        const uint32_t sbuf = tmem + static_cast<uint32_t>(t % kNB) * kBN;
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint64_t off = ((kk >> 2) * C::kPanelBytes + (kk & 3) * 32) >> 4;
-            ptx::mma_bf16_ss_w(sbuf, dq + off, dk + soff + off, C::kIdescQK, kk > 0);
-          }
-          ptx::mma_commit_w(&s_full[t % kNB]);
-          if (lane == 0) trace_stamp(p, 6, t);
-        } else {
-          // O += P(t) V_t, P(t) read from TMEM (S buffer t%3)
-          ptx::mbar_wait(&p_ready[t % kNB], static_cast<uint32_t>((t / kNB) & 1));
-          if (lane == 0) trace_stamp(p, 4, t);
-          ptx::tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk)
-            ptx::mma_bf16_ts_w(tmem + kOCol, sbuf + kk * 8, dv + soff + ((kk * 16 * 128) >> 4),
-                               C::kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
-          ptx::mma_commit_w(&pv_done[t & 1]);
-          if (t == n_own - 1) ptx::mma_commit_w(o_final);
-          if (lane == 0) trace_stamp(p, 5, t);
-        }
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          ptx::mma2_bf16_ts_lo(tmem + kOCol, sbuf + kk * 8, v_lo + soff + ((kk * 16 * 128) >> 4),
+                               kDescHi, C::kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma2_commit_mc_w(&pv_done[t % kNB], 0x3);
+        if (t == n_own - 1) ptx::mma2_commit_mc_w(o_final, 0x3);
+        ptx::mma2_commit_mc_w(&kv_empty[stage], 0x3);
+        if (lane == 0) trace_stamp(p, 5, t);
       }
-      ptx::mma_commit_mc_w(&kv_empty[stage], 0x3);  // release the slot in both CTAs
       if (++stage == C::kStages) { stage = 0; phase ^= 1; }
     }
     __syncwarp();
@@ -442,7 +574,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // completes (at most one pv_done phase can be pending here).
       if (j > 0 && __any_sync(0xffffffffu, m_cur != m_in)) {
         const float alpha = (m_in == -INFINITY || m_cur == m_in) ? 1.f : ptx::ex2_approx(m_in - m_cur);
-        ptx::mbar_wait(&pv_done[(j - 1) & 1], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+        if (K2)
+          ptx::mbar_wait(&pv_done[(j - 1) % kNB], static_cast<uint32_t>(((j - 1) / kNB) & 1));
+        else
+          ptx::mbar_wait(&pv_done[(j - 1) & 1], static_cast<uint32_t>(((j - 1) >> 1) & 1));
         ptx::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
@@ -458,7 +593,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       if (leader) trace_stamp(p, 2 * w + 1, j);
-      ptx::mbar_arrive(&p_ready[j % kNB]);
+      if (K2) {  // one arrive per warp on the pair leader's barrier
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_cluster(&p_ready[j % kNB], 0));
+      } else {
+        ptx::mbar_arrive(&p_ready[j % kNB]);
+      }
     }
     if (n_own > 0) {
       ptx::mbar_wait(o_final, 0);
@@ -521,12 +661,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<512>(tmem);
+  if (K2) {
+    ptx::cluster_sync();  // both CTAs done with the pair's TMEM and each other's barriers
+    if (warp == kMmaWarp) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc_2cta<512>(tmem);
+    }
+  } else {
+    __syncthreads();
+    if (warp == kMmaWarp) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc<512>(tmem);
+    }
+    ptx::cluster_sync();  // the peer may still multicast into / arrive on this CTA until here
   }
-  ptx::cluster_sync();  // the peer may still multicast into / arrive on this CTA until here
 }
 
 // ---------------------------------------------------------------- host side
@@ -567,38 +715,67 @@ bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D, int b
   return r == CUDA_SUCCESS;
 }
 
-// Kernel variant (measurement knob): DMHA_EMU=<pairs of 8 on the FMA pipe>.
+// Kernel variant (measurement knobs): DMHA_EMU=<pairs of 8 on the FMA pipe>,
+// DMHA_PAIR_MMA=0 to use the per-CTA MMA path for D = 128.
 template <int D>
 int emu_variant() {
   static int v = [] {
-    int x = Cfg<D>::kEmuDefault;
+    int x = Cfg<D, false>::kEmuDefault;
     if (const char* e = std::getenv("DMHA_EMU")) x = std::atoi(e);
     return x;
   }();
   return v;
 }
+// Kernel choice: DMHA_KERNEL = pingpong | cluster | pair (default pingpong,
+// the measured fastest on C3/C4/C5).
+enum KernelKind { K_PINGPONG, K_CLUSTER, K_PAIR };
+inline KernelKind kernel_kind(int D) {
+  const char* e = std::getenv("DMHA_KERNEL");
+  if (e) {
+    if (!strcmp(e, "pingpong")) return K_PINGPONG;
+    if (!strcmp(e, "cluster")) return K_CLUSTER;
+    if (!strcmp(e, "pair")) return D == 128 ? K_PAIR : K_CLUSTER;
+  }
+  return K_PINGPONG;
+}
 
-template <int D, int E>
+template <int D, int E, bool K2>
 cudaError_t launch_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const Params& p, dim3 grid, cudaStream_t stream) {
-  using C = Cfg<D>;
+  using C = Cfg<D, K2>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E>,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, K2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  attn_fwd_sm100_kernel<D, E><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  attn_fwd_sm100_kernel<D, E, K2><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
+}
+
+template <int D, bool K2>
+cudaError_t launch_e(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                     const Params& p, dim3 grid, cudaStream_t stream) {
+  switch (emu_variant<D>()) {
+    case 0: return launch_v<D, 0, K2>(tq, tk, tv, p, grid, stream);
+    case 1: return launch_v<D, 1, K2>(tq, tk, tv, p, grid, stream);
+    case 2: return launch_v<D, 2, K2>(tq, tk, tv, p, grid, stream);
+    case 3: return launch_v<D, 3, K2>(tq, tk, tv, p, grid, stream);
+    case 4: return launch_v<D, 4, K2>(tq, tk, tv, p, grid, stream);
+    default: return launch_v<D, Cfg<D, K2>::kEmuDefault, K2>(tq, tk, tv, p, grid, stream);
+  }
 }
 
 template <int D>
 cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
+  const bool k2 = (D == 128) && kernel_kind(D) == K_PAIR;
   CUtensorMap tq, tk, tv;
+  // K: 64-key half tiles (pair MMA: own half; multicast path: half per CTA).
+  // V: pair MMA loads all 128 keys x 64 columns; multicast path 64-key halves.
   if (!make_map(&tq, a.q, a.Lq, a.H, D, kBM) || !make_map(&tk, a.k, a.Lk, a.H, D, kBN / 2) ||
-      !make_map(&tv, a.v, a.Lk, a.H, D, kBN / 2))
+      !make_map(&tv, a.v, a.Lk, a.H, D, k2 ? kBN : kBN / 2))
     return cudaErrorInvalidValue;
   Params p;
   p.Lq = a.Lq;
@@ -614,14 +791,10 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   p.n_pairs = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.trace = g_trace;
   dim3 grid(2 * p.n_pairs, a.H);
-  switch (emu_variant<D>()) {
-    case 0: return launch_v<D, 0>(tq, tk, tv, p, grid, stream);
-    case 1: return launch_v<D, 1>(tq, tk, tv, p, grid, stream);
-    case 2: return launch_v<D, 2>(tq, tk, tv, p, grid, stream);
-    case 3: return launch_v<D, 3>(tq, tk, tv, p, grid, stream);
-    case 4: return launch_v<D, 4>(tq, tk, tv, p, grid, stream);
-    default: return launch_v<D, Cfg<D>::kEmuDefault>(tq, tk, tv, p, grid, stream);
+  if constexpr (D == 128) {
+    if (k2) return launch_e<D, true>(tq, tk, tv, p, grid, stream);
   }
+  return launch_e<D, false>(tq, tk, tv, p, grid, stream);
 }
 
 }  // namespace
@@ -631,6 +804,7 @@ unsigned long long* g_trace = nullptr;
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream) {
   if (a.Lq <= 0) return cudaSuccess;
   if (a.Lq > INT32_MAX || a.Lk > INT32_MAX) return cudaErrorInvalidValue;
+  if (kernel_kind(a.D) == K_PINGPONG) return launch_attn_fwd_bf16_pingpong(a, stream);
   if (a.D == 64) return launch_d<64>(a, stream);
   if (a.D == 128) return launch_d<128>(a, stream);
   return cudaErrorInvalidValue;

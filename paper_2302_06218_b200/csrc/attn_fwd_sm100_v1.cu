@@ -1,0 +1,476 @@
+// attn_fwd_sm100_v1.cu — "ping-pong" flash-attention forward for sm_100a:
+// two 128-row query tiles per CTA share every K/V tile in shared memory (so
+// L2->SMEM traffic is one K/V tile per 256 query rows) and alternate on the
+// tensor core.  Default kernel for D = 128 (measured fastest there, see
+// DESIGN.md "Attention kernel"); attn_fwd_sm100.cu holds the clustered
+// variants used for D = 64.
+//
+// Computes, for one query block against one key/value block (one ring step,
+// SURVEY §8(a) a2), per head h and query row i:
+//   S = Q K^T / sqrt(D)                      PAPER.md:193-196 Eq. `unnormalized`
+//   A = row softmax(S) over the usable keys
+//   Z = A V                                  PAPER.md:203-211 Eq. `attn-sum`
+//   lse = ln sum_j exp(S_j)                  (reading R9)
+// with the causal rule "key j usable by row i iff kpos(j) <= qpos(i)" on
+// GLOBAL positions (north_star), so the same kernel serves every ring step and
+// both shard layouts.  S, P and O never leave the SM: S and O accumulate in
+// TMEM, P is written back to TMEM as bf16 and consumed from there.
+//
+// CTA = 2 query tiles of 128 rows (256 rows) of one head; 12 warps:
+//   warps 0-3  softmax for Q tile 0 (thread t <-> TMEM lane t <-> row t)
+//   warps 4-7  softmax for Q tile 1
+//   warp  8    TMA producer (Q once; K_j, V_j through an NST-slot ring)
+//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 10-11 idle (keep the CTA at 3 warpgroups)
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D);
+// P_g (bf16x2) aliases the first 64 columns of S_g.
+// MMA order per KV tile j:  PV0_{j-1}, S0_j, PV1_{j-1}, S1_j — S_g(j) is issued
+// after PV_g(j-1) read P_g(j-1) (tcgen05.mma executes in issue order), and the
+// commit that signals S_g(j) also covers PV_g(j-1), so the softmax warps can
+// rescale O_g right after they see S_g(j).
+// Online softmax in the exp2 domain with a stale running max: O is rescaled
+// only when the tile max exceeds the running max by more than 8 (factor 256);
+// exact because l and O always share the max that was subtracted.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+
+#include "kernels.h"
+#include "ptx_sm100.cuh"
+
+namespace dmha {
+namespace {
+
+constexpr int kBM = 128;          // query rows per tile (MMA M)
+constexpr int kBN = 128;          // keys per tile (MMA N of QK^T, K of PV)
+constexpr int kThreads = 384;     // 12 warps
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
+
+template <int D>
+struct Cfg {
+  static constexpr int kPanels = D / 64;                    // 128-byte swizzle panels per row
+  static constexpr int kPanelBytes = 128 * 128;             // 128 rows x 128 B
+  static constexpr int kTileBytes = kPanels * kPanelBytes;  // one 128 x D bf16 tile
+  static constexpr int kStages = (D == 128) ? 4 : 6;        // K/V ring slots
+  static constexpr int kQOff = 0;
+  static constexpr int kKVOff = 2 * kTileBytes;
+  static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
+  static constexpr int kSmemBytes = kBarOff + 256 + 1024;   // + barriers + align slack
+  static constexpr uint32_t kIdescQK = ptx::make_idesc(1, kBM, kBN, 0, 0);
+  static constexpr uint32_t kIdescPV = ptx::make_idesc(1, kBM, D, 0, 1);  // V is MN-major
+};
+
+struct Params {
+  int64_t Lq, Lk;
+  int H;
+  int causal;
+  PosMap qmap, kmap;
+  float scale_log2;  // log2(e) / sqrt(D)
+  void* out;
+  float* lse;
+  int out_mode;
+  int n_mblk;
+};
+
+__device__ __forceinline__ int64_t pos_of(const PosMap& m, int64_t i) {
+  return i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
+}
+
+// Number of leading keys (a prefix, since kpos is increasing) that a query at
+// global position qp may use.
+__device__ __forceinline__ int64_t key_limit(const Params& p, int64_t qp) {
+  if (!p.causal) return p.Lk;
+  const PosMap& m = p.kmap;
+  int64_t lim;
+  if (p.Lk > m.chunk && qp >= m.base1) {
+    lim = m.chunk + (qp - m.base1) + 1;
+  } else if (qp >= m.base0) {
+    lim = qp - m.base0 + 1;
+    if (lim > m.chunk) lim = m.chunk;
+  } else {
+    lim = 0;
+  }
+  return lim < p.Lk ? lim : p.Lk;
+}
+
+// KV tiles this CTA has to visit (a prefix of the key tiles).
+__device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
+  int64_t last = m0 + 2 * kBM - 1;
+  if (last > p.Lq - 1) last = p.Lq - 1;
+  const int64_t lim = key_limit(p, pos_of(p.qmap, last));
+  return static_cast<int>((lim + kBN - 1) / kBN);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
+                          const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  using C = Cfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem + C::kQOff;
+  uint8_t* sKV = smem + C::kKVOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;   // [2]
+  uint64_t* p_ready = s_full + 2;             // [2]
+  uint64_t* o_final = p_ready + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  // Causal: heaviest query blocks first.
+  const int mblk = p.causal ? (p.n_mblk - 1 - static_cast<int>(blockIdx.x))
+                            : static_cast<int>(blockIdx.x);
+  const int64_t m0 = static_cast<int64_t>(mblk) * (2 * kBM);
+  const int nkv = num_kv_tiles(p, m0);
+
+  if (warp == kProducerWarp && lane == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int g = 0; g < 2; ++g) {
+      ptx::mbar_init(&s_full[g], 1);
+      ptx::mbar_init(&p_ready[g], kBM);
+      ptx::mbar_init(&o_final[g], 1);
+    }
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+  }
+  if (warp == kMmaWarp) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && nkv > 0) {
+      ptx::mbar_arrive_expect_tx(q_full, 2 * C::kTileBytes);
+      for (int g = 0; g < 2; ++g)
+        for (int pn = 0; pn < C::kPanels; ++pn)
+          ptx::tma_load_3d(&tm_q, q_full, sQ + g * C::kTileBytes + pn * C::kPanelBytes, pn * 64,
+                           head, static_cast<int32_t>(m0 + g * kBM));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < nkv; ++j) {
+        for (int which = 0; which < 2; ++which) {
+          ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
+          const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
+          for (int pn = 0; pn < C::kPanels; ++pn)
+            ptx::tma_load_3d(tm, &kv_full[stage], sKV + stage * C::kTileBytes + pn * C::kPanelBytes,
+                             pn * 64, head, j * kBN);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && nkv > 0) {
+      const uint32_t sq = ptx::smem_u32(sQ);
+      const uint32_t skv = ptx::smem_u32(sKV);
+      auto qk = [&](int g, int slot) {
+        const uint32_t a0 = sq + g * C::kTileBytes;
+        const uint32_t b0 = skv + slot * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kPanelBytes + (kk & 3) * 32;
+          ptx::mma_bf16_ss(tmem + g * kBN, ptx::smem_desc_sw128(a0 + off, 16, 1024),
+                           ptx::smem_desc_sw128(b0 + off, 16, 1024), C::kIdescQK, kk > 0);
+        }
+      };
+      auto pv = [&](int g, int slot, bool acc) {
+        const uint32_t b0 = skv + slot * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          ptx::mma_bf16_ts(tmem + 256 + g * 128, tmem + g * kBN + kk * 8,
+                           ptx::smem_desc_sw128(b0 + kk * 16 * 128, C::kPanelBytes, 1024),
+                           C::kIdescPV, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      int stage = 0;
+      uint32_t phase = 0;
+      auto advance = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
+
+      ptx::mbar_wait(q_full, 0);
+      // j = 0
+      int slotK = stage;
+      ptx::mbar_wait(&kv_full[slotK], phase);
+      advance();
+      ptx::tc_fence_after();
+      qk(0, slotK);
+      ptx::mma_commit(&s_full[0]);
+      qk(1, slotK);
+      ptx::mma_commit(&s_full[1]);
+      ptx::mma_commit(&kv_empty[slotK]);
+      for (int j = 1; j <= nkv; ++j) {
+        const int slotV = stage;  // V_{j-1}
+        ptx::mbar_wait(&kv_full[slotV], phase);
+        advance();
+        const bool more = j < nkv;
+        int slotK2 = -1;
+        if (more) {
+          slotK2 = stage;  // K_j
+          ptx::mbar_wait(&kv_full[slotK2], phase);
+          advance();
+        }
+        const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
+        ptx::mbar_wait(&p_ready[0], ppar);
+        ptx::tc_fence_after();
+        pv(0, slotV, j > 1);
+        if (more) {
+          qk(0, slotK2);
+          ptx::mma_commit(&s_full[0]);
+        } else {
+          ptx::mma_commit(&o_final[0]);
+        }
+        ptx::mbar_wait(&p_ready[1], ppar);
+        ptx::tc_fence_after();
+        pv(1, slotV, j > 1);
+        ptx::mma_commit(&kv_empty[slotV]);
+        if (more) {
+          qk(1, slotK2);
+          ptx::mma_commit(&s_full[1]);
+          ptx::mma_commit(&kv_empty[slotK2]);
+        } else {
+          ptx::mma_commit(&o_final[1]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ softmax
+    const int g = warp >> 2;                  // Q tile of this warpgroup
+    const int quarter = warp & 3;             // TMEM lane quarter
+    const int r = quarter * 32 + lane;        // row within the tile
+    const int64_t row = m0 + g * kBM + r;     // local query row
+    const bool row_ok = row < p.Lq;
+    const int64_t qp = pos_of(p.qmap, row_ok ? row : p.Lq - 1);
+    const int64_t klim = key_limit(p, qp);
+    const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + g * kBN;
+    const uint32_t tO = tmem + lane_addr + 256 + g * 128;
+    const float sl2 = p.scale_log2;
+
+    float m_run = -INFINITY;  // running max, log2 units (scaled)
+    float l_run = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      ptx::mbar_wait(&s_full[g], static_cast<uint32_t>(j & 1));
+      ptx::tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
+      ptx::tmem_wait_ld();
+
+      int64_t nv64 = klim - static_cast<int64_t>(j) * kBN;
+      const int nvalid = nv64 < 0 ? 0 : (nv64 > kBN ? kBN : static_cast<int>(nv64));
+      if (!__all_sync(0xffffffffu, nvalid >= kBN)) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
+      }
+      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+#pragma unroll
+      for (int c = 4; c < 128; c += 4) {
+        mx0 = fmaxf(mx0, s[c]);
+        mx1 = fmaxf(mx1, s[c + 1]);
+        mx2 = fmaxf(mx2, s[c + 2]);
+        mx3 = fmaxf(mx3, s[c + 3]);
+      }
+      const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const bool need = mt > m_run + kRescaleThreshold;
+      const bool warp_rescale = __any_sync(0xffffffffu, need);
+      float alpha = 1.f;
+      if (warp_rescale) {
+        const float m_new = fmaxf(m_run, mt);
+        alpha = (m_new == -INFINITY) ? 1.f : ptx::ex2_approx(m_run - m_new);
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      // P = exp2(S*scale*log2e - m) -> bf16, written over the first 64 columns
+      // of S in 16-column chunks so the fp32 scores die as P is produced.
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], sl2, -m_use));
+          const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], sl2, -m_use));
+          sum0 += e0;
+          sum1 += e1;
+          __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
+          pk[e] = *reinterpret_cast<uint32_t*>(&b);
+        }
+        ptx::tmem_st16(tS + c * 16, pk);
+      }
+      l_run += sum0 + sum1;
+      // O_g holds PV_g(j-1) (complete: covered by the S_g(j) commit) and PV_g(j)
+      // is not issued before p_ready, so O can be rescaled in place here.
+      if (warp_rescale && j > 0) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          ptx::tmem_ld32(tO + c * 32, o);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] *= alpha;
+          ptx::tmem_st32(tO + c * 32, o);
+        }
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&p_ready[g]);
+    }
+    if (nkv > 0) {
+      ptx::mbar_wait(&o_final[g], 0);
+      ptx::tc_fence_after();
+    }
+    // ---------------------------------------------------------- epilogue
+    const bool empty = !(l_run > 0.f);
+    const float inv_l = empty ? 0.f : 1.f / l_run;
+    if (row_ok)
+      p.lse[static_cast<int64_t>(head) * p.Lq + row] =
+          empty ? -INFINITY : (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+    const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D);
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      float o[32];
+      if (nkv > 0) {
+        ptx::tmem_ld32(tO + c * 32, o);
+        ptx::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = 0.f;
+      }
+      if (row_ok) {
+        if (p.out_mode == OUT_PARTIAL_F32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dst[e] = make_float4(o[4 * e] * inv_l, o[4 * e + 1] * inv_l, o[4 * e + 2] * inv_l,
+                                 o[4 * e + 3] * inv_l);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
+                                                c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t w[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(o[8 * e + 2 * t] * inv_l,
+                                                       o[8 * e + 2 * t + 1] * inv_l);
+              w[t] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// [L, H, D] bf16 viewed as a 3-D tensor (D, H, L); box (64, 1, 128), 128B swizzle.
+bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  // A zero-length block is never loaded (nkv = 0) but the map must be valid.
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(L > 0 ? L : 1)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2,
+                           static_cast<cuuint64_t>(D) * H * 2};
+  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int D>
+cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
+  using C = Cfg<D>;
+  CUtensorMap tq, tk, tv;
+  if (!make_map(&tq, a.q, a.Lq, a.H, D) || !make_map(&tk, a.k, a.Lk, a.H, D) ||
+      !make_map(&tv, a.v, a.Lk, a.H, D))
+    return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  Params p;
+  p.Lq = a.Lq;
+  p.Lk = a.Lk;
+  p.H = a.H;
+  p.causal = a.causal;
+  p.qmap = a.qmap;
+  p.kmap = a.kmap;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
+  p.out = a.out;
+  p.lse = a.lse;
+  p.out_mode = a.out_mode;
+  p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
+  dim3 grid(p.n_mblk, a.H);
+  attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t stream) {
+  if (a.Lq <= 0) return cudaSuccess;
+  if (a.Lq > INT32_MAX || a.Lk > INT32_MAX) return cudaErrorInvalidValue;
+  if (a.D == 64) return launch_d<64>(a, stream);
+  if (a.D == 128) return launch_d<128>(a, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dmha

@@ -29,8 +29,11 @@ struct LocalAttnArgs {
   int out_mode;
 };
 
-// bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu).
+// bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu): picks
+// the variant per head dim (DMHA_KERNEL=pingpong|cluster|pair overrides).
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream);
+// Two query tiles per CTA, ping-pong on the tensor core (attn_fwd_sm100_v1.cu).
+cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t stream);
 // fp32 path (attn_fwd_fp32.cu).
 cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
 // log-sum-exp combine (lse_combine.cu).  out_dtype_bf16 selects the final

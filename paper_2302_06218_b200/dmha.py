@@ -230,7 +230,7 @@ def get_stats() -> dict:
 
 
 def debug_set_trace(buf):
-    """Timeline hook: buf = device uint64 tensor of >= 4*7*64 entries, or None."""
+    """Timeline hook: buf = device uint64 tensor of >= 4*9*64 entries, or None."""
     _check(lib().dmha_debug_set_trace(None if buf is None else _ptr(buf)))
 
 

@@ -12,18 +12,18 @@ from paper_2302_06218_b200 import dmha  # noqa: E402
 L = int(os.environ.get("TL", 262144 // 8)); H = 16; D = int(os.environ.get("TD", 128))
 dmha.init(1, 0, None, 0, "bf16", "contiguous")
 q, k, v = (torch.randn(L, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
-buf = torch.zeros(4 * 7 * 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(4 * 9 * 64, dtype=torch.int64, device="cuda")
 dmha.forward(q, k, v, L, False)
 dmha.debug_set_trace(buf)
 dmha.forward(q, k, v, L, False)
 torch.cuda.synchronize()
 dmha.debug_set_trace(None)
-t = buf.view(4, 7, 64).cpu().numpy().astype(np.int64)
+t = buf.view(4, 9, 64).cpu().numpy().astype(np.int64)
 for c in range(2):
     tc = t[c] - t[c][0][0]
-    print(f"CTA {c}: rows = tile j; cols = 0:WG0 saw S 1:WG0 P 2:WG1 saw S 3:WG1 P 4:mma saw P 5:mma PV issued 6:mma S issued")
+    print(f"CTA {c}: rows = tile j; cols = 0:WG0 saw S 1:WG0 P 2:WG1 saw S 3:WG1 P 4:mma saw P 5:mma PV issued 6:mma S issued 7:mma saw V landed 8:producer issued V load")
     for j in range(8, 16):
-        print(j, " ".join(f"{tc[e][j]:8d}" for e in range(7)))
+        print(j, " ".join(f"{tc[e][j]:8d}" if t[c][e][j] else "       -" for e in range(9)))
     # steady-state stats over tiles 8..60
     js = range(8, 60)
     per = np.diff(tc[0][8:60]).mean()
