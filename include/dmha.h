@@ -145,6 +145,30 @@ int dmha_set_profiling(int enable);
 
 /* ---- individual hot-path steps (exported for tests and the bench) ------- */
 
+/* a1/a3 (north_star (3)): what rank `rank` does at ring step `step`
+ * (0 <= step < world_size).  Pure host function of its arguments; dmha_forward
+ * and dmha_forward_emulated follow exactly this plan. */
+enum dmha_plan_output {
+  DMHA_PLAN_FINAL = 0,          /* P == 1: attention writes out/lse directly       */
+  DMHA_PLAN_ACC = 1,            /* step 0: attention writes the fp32 accumulator   */
+  DMHA_PLAN_COMBINE = 2,        /* partial, then LSE-combine into the accumulator  */
+  DMHA_PLAN_COMBINE_FINAL = 3   /* last step: combine writes out (bf16/fp32) + lse */
+};
+struct dmha_ring_plan {
+  int src;                   /* rank whose K/V block is attended to at this step      */
+  int send_to;               /* rank the current K/V block is sent to (-1: none)       */
+  int recv_from;             /* rank the next block is received from (-1: none)        */
+  int compute_buf;           /* K/V used: -1 = caller's k/v, else ring buffer 0/1      */
+  int recv_buf;              /* ring buffer the next block lands in (-1: none)         */
+  int recv_after_compute_of; /* the receive waits for this step's compute (-1: none)   */
+  int output;                /* enum dmha_plan_output                                  */
+  int64_t q_base0, q_base1, q_chunk; /* global position map of this rank's rows   */
+  int64_t k_base0, k_base1, k_chunk; /* ... and of the src rank's K/V rows         */
+};
+int dmha_ring_plan_step(int world_size, int rank, int step, int layout, int64_t L,
+                        struct dmha_ring_plan *plan_out);
+
+
 /* a1: global sequence position of local row i of rank r for
  * (L, P, layout).  Pure host index math. Returns INVALID on bad arguments. */
 int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_t i,

@@ -312,21 +312,50 @@ int run_combine(float* o_part, float* lse_part, void* out, float* lse, int64_t L
   return DMHA_OK;
 }
 
+// The ring schedule of rank r at step s.  Pure function of
+// (P, r, s, layout, L): shared by the NCCL ring, the single-GPU emulation and
+// (exported as dmha_ring_plan) the multi-process CPU tests.
+dmha_ring_plan make_plan(int P, int r, int s, int layout, int64_t L) {
+  dmha_ring_plan pl;
+  pl.src = ((r - s) % P + P) % P;
+  pl.send_to = s < P - 1 ? (r + 1) % P : -1;
+  pl.recv_from = s < P - 1 ? (r - 1 + P) % P : -1;
+  pl.compute_buf = s == 0 ? -1 : (s & 1);
+  pl.recv_buf = s < P - 1 ? ((s + 1) & 1) : -1;
+  pl.recv_after_compute_of = (s < P - 1 && s >= 2) ? s - 1 : -1;
+  pl.output = P == 1 ? DMHA_PLAN_FINAL : (s == 0 ? DMHA_PLAN_ACC : (s == P - 1 ? DMHA_PLAN_COMBINE_FINAL
+                                                                              : DMHA_PLAN_COMBINE));
+  const dmha::PosMap qm = posmap(L, P, r, layout), km = posmap(L, P, pl.src, layout);
+  pl.q_base0 = qm.base0;
+  pl.q_base1 = qm.base1;
+  pl.q_chunk = qm.chunk;
+  pl.k_base0 = km.base0;
+  pl.k_base1 = km.base1;
+  pl.k_chunk = km.chunk;
+  return pl;
+}
+
 // Compute part of ring step s for rank r (shared by the NCCL and emulated rings
 // so both run identical kernels in identical order).
 int ring_compute_step(int s, int P, int r, int layout, const void* q, const void* ks,
                       const void* vs, void* out, float* lse, int64_t L, int D, int H, int causal) {
   const int64_t Lloc = L / P;
-  const int src = ((r - s) % P + P) % P;
-  const dmha::PosMap qm = posmap(L, P, r, layout), km = posmap(L, P, src, layout);
-  if (P == 1) return run_local(q, ks, vs, out, lse, Lloc, Lloc, D, H, causal, qm, km, dmha::OUT_FINAL);
-  if (s == 0)
-    return run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
-                     dmha::OUT_PARTIAL_F32);
-  int rc = run_local(q, ks, vs, g.o_part, g.lse_part, Lloc, Lloc, D, H, causal, qm, km,
-                     dmha::OUT_PARTIAL_F32);
-  if (rc) return rc;
-  return run_combine(g.o_part, g.lse_part, out, lse, Lloc, D, H, s == P - 1);
+  const dmha_ring_plan pl = make_plan(P, r, s, layout, L);
+  const dmha::PosMap qm{pl.q_base0, pl.q_base1, pl.q_chunk}, km{pl.k_base0, pl.k_base1, pl.k_chunk};
+  switch (pl.output) {
+    case DMHA_PLAN_FINAL:
+      return run_local(q, ks, vs, out, lse, Lloc, Lloc, D, H, causal, qm, km, dmha::OUT_FINAL);
+    case DMHA_PLAN_ACC:
+      return run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
+                       dmha::OUT_PARTIAL_F32);
+    default: {
+      int rc = run_local(q, ks, vs, g.o_part, g.lse_part, Lloc, Lloc, D, H, causal, qm, km,
+                         dmha::OUT_PARTIAL_F32);
+      if (rc) return rc;
+      return run_combine(g.o_part, g.lse_part, out, lse, Lloc, D, H,
+                         pl.output == DMHA_PLAN_COMBINE_FINAL);
+    }
+  }
 }
 
 int poll_nccl() {
@@ -464,6 +493,18 @@ int dmha_set_profiling(int enable) {
   return DMHA_OK;
 }
 
+int dmha_ring_plan_step(int world_size, int rank, int step, int layout, int64_t L,
+                        struct dmha_ring_plan* plan_out) {
+  if (!plan_out || world_size < 1 || rank < 0 || rank >= world_size || step < 0 ||
+      step >= world_size || L < 1)
+    return fail(DMHA_ERR_INVALID, "dmha_ring_plan_step: bad args");
+  const int64_t div = layout == DMHA_LAYOUT_ZIGZAG ? 2LL * world_size : world_size;
+  if ((layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG) || L % div)
+    return fail(DMHA_ERR_INVALID, "dmha_ring_plan_step: bad layout or L");
+  *plan_out = make_plan(world_size, rank, step, layout, L);
+  return DMHA_OK;
+}
+
 int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_t i,
                          int64_t* global_out) {
   if (!global_out || world_size < 1 || rank < 0 || rank >= world_size || L < 1)
@@ -493,22 +534,23 @@ int dmha_forward(const void* q, const void* k, const void* v, void* out, float* 
   const int64_t Lloc = L / P;
   if (int rc = ensure_ring_ws(Lloc, D, H, true)) return rc;
   const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
-  const int next = (r + 1) % P, prev = (r - 1 + P) % P;
   CK_CUDA(cudaEventRecord(g.ev_start, g.stream));
   CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_start, 0));
   const void* kcur = k;
   const void* vcur = v;
   for (int s = 0; s < P; ++s) {
-    if (s < P - 1) {
-      const int nb = (s + 1) & 1;
-      if (s >= 2) CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_done[nb], 0));
+    const dmha_ring_plan pl = make_plan(P, r, s, g.layout, L);
+    if (pl.recv_buf >= 0) {
+      const int nb = pl.recv_buf;
+      // the buffer's last reader was the compute of step s-1
+      if (pl.recv_after_compute_of >= 0) CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_done[nb], 0));
       char* dst = static_cast<char*>(g.kvbuf[nb]);
       int rc = timed(2, g.comm, [&]() {
         CK_NCCL(ncclGroupStart());
-        CK_NCCL(ncclSend(kcur, blk, ncclChar, next, g.nccl, g.comm));
-        CK_NCCL(ncclSend(vcur, blk, ncclChar, next, g.nccl, g.comm));
-        CK_NCCL(ncclRecv(dst, blk, ncclChar, prev, g.nccl, g.comm));
-        CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, prev, g.nccl, g.comm));
+        CK_NCCL(ncclSend(kcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
+        CK_NCCL(ncclSend(vcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
+        CK_NCCL(ncclRecv(dst, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
+        CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
         CK_NCCL(ncclGroupEnd());
         return static_cast<int>(DMHA_OK);
       });
@@ -518,10 +560,10 @@ int dmha_forward(const void* q, const void* k, const void* v, void* out, float* 
     }
     int rc = ring_compute_step(s, P, r, g.layout, q, kcur, vcur, out, lse, L, D, H, causal);
     if (rc) return rc;
-    if (s >= 1) CK_CUDA(cudaEventRecord(g.ev_done[s & 1], g.stream));
+    if (pl.compute_buf >= 0) CK_CUDA(cudaEventRecord(g.ev_done[pl.compute_buf], g.stream));
     g.stats.ring_steps++;
-    if (s < P - 1) {
-      const int nb = (s + 1) & 1;
+    if (pl.recv_buf >= 0) {
+      const int nb = pl.recv_buf;
       CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_recv[nb], 0));
       kcur = g.kvbuf[nb];
       vcur = static_cast<char*>(g.kvbuf[nb]) + blk;
@@ -592,7 +634,7 @@ int dmha_forward_emulated(int world_size, int layout, const void* q, const void*
     char* outr = static_cast<char*>(out) + r * blk;
     float* lser = lse + static_cast<size_t>(r) * Lloc * H;
     for (int s = 0; s < P; ++s) {
-      const int src = ((r - s) % P + P) % P;
+      const int src = make_plan(P, r, s, layout, L).src;
       const char* ks = static_cast<const char*>(k) + src * blk;
       const char* vs = static_cast<const char*>(v) + src * blk;
       if (int rc = ring_compute_step(s, P, r, layout, qr, ks, vs, outr, lser, L, D, H, causal)) return rc;

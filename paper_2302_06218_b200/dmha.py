@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "dmha_get_unique_id", "dmha_init", "dmha_set_stream", "dmha_finalize", "dmha_last_error",
     "dmha_forward", "dmha_forward_host", "dmha_forward_emulated", "dmha_workspace_bytes",
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
-    "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace",
+    "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
 )
 
 
@@ -44,6 +44,16 @@ class Stats(ctypes.Structure):
                 ("attn_ms", ctypes.c_double), ("combine_ms", ctypes.c_double),
                 ("exchange_ms", ctypes.c_double)]
 
+
+class RingPlan(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_int), ("send_to", ctypes.c_int), ("recv_from", ctypes.c_int),
+                ("compute_buf", ctypes.c_int), ("recv_buf", ctypes.c_int),
+                ("recv_after_compute_of", ctypes.c_int), ("output", ctypes.c_int),
+                ("q_base0", ctypes.c_int64), ("q_base1", ctypes.c_int64), ("q_chunk", ctypes.c_int64),
+                ("k_base0", ctypes.c_int64), ("k_base1", ctypes.c_int64), ("k_chunk", ctypes.c_int64)]
+
+
+PLAN_FINAL, PLAN_ACC, PLAN_COMBINE, PLAN_COMBINE_FINAL = 0, 1, 2, 3
 
 _lib = None
 
@@ -72,6 +82,7 @@ def lib():
             "dmha_synchronize": [],
             "dmha_set_profiling": [I],
             "dmha_debug_set_trace": [P],
+            "dmha_ring_plan_step": [I, I, I, I, I64, ctypes.POINTER(RingPlan)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -243,6 +254,14 @@ def local_to_global(L: int, world_size: int, rank: int, layout, i: int) -> int:
     _check(lib().dmha_local_to_global(int(L), int(world_size), int(rank), layout_code(layout),
                                       int(i), ctypes.byref(g)))
     return g.value
+
+
+def ring_plan(world_size: int, rank: int, step: int, layout, L: int) -> dict:
+    """The library's ring schedule for (rank, step): a plain dict of RingPlan fields."""
+    pl = RingPlan()
+    _check(lib().dmha_ring_plan_step(int(world_size), int(rank), int(step), layout_code(layout),
+                                     int(L), ctypes.byref(pl)))
+    return {f: int(getattr(pl, f)) for f, _ in RingPlan._fields_}
 
 
 def global_rows(L: int, world_size: int, rank: int, layout) -> np.ndarray:

@@ -232,3 +232,30 @@ def test_error_codes(lib_bf16):
         dmha.forward_emulated(3, "contiguous", *(torch.zeros((3, 10, 2, 64), dtype=torch.bfloat16,
                                                             device="cuda") for _ in range(3)), 31, False)
     assert e.value.code == dmha.ERR_INVALID
+
+
+@pytest.mark.parametrize("kernel", ["pingpong", "cluster", "pair"])
+@pytest.mark.parametrize("L,H,D,causal", [(1000, 2, 128, False), (2085, 2, 64, True), (777, 3, 128, True),
+                                          (4096, 1, 128, False), (300, 1, 64, False)])
+def test_kernel_variants_parity(lib_bf16, oracle_mod, monkeypatch, kernel, L, H, D, causal):
+    """Every attention kernel variant (DMHA_KERNEL) against the oracle."""
+    monkeypatch.setenv("DMHA_KERNEL", kernel)
+    q, k, v = inputs.qkv(L, H, D, seed=3000 + L + D)
+    out, lse = run_p1(q, k, v, causal)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(out, lse, ref_o, ref_l, "bf16", f"{kernel} L={L} H={H} D={D} causal={causal}")
+
+
+@pytest.mark.parametrize("kernel", ["pingpong", "cluster", "pair"])
+def test_kernel_variants_ring_partials(lib_bf16, oracle_mod, monkeypatch, kernel):
+    """Variants on the ring path (global-position masks, fp32 partials, zigzag)."""
+    monkeypatch.setenv("DMHA_KERNEL", kernel)
+    P, L, H, D = 4, 2048, 2, 128
+    q, k, v = inputs.qkv(L, H, D, seed=77)
+    parts = [np.stack([dmha.shard(x, P, r, "zigzag") for r in range(P)]) for x in (q, k, v)]
+    out, lse = dmha.forward_emulated(P, "zigzag", *(to_dev(p) for p in parts), L, True)
+    torch.cuda.synchronize()
+    og = dmha.unshard(list(out.float().cpu().numpy()), L, "zigzag")
+    lg = dmha.unshard([x.T for x in lse.cpu().numpy()], L, "zigzag").T
+    ref_o, ref_l = oracle_mod.attention(q, k, v, True)
+    assert_parity(og, lg, ref_o, ref_l, "bf16", f"{kernel} ring")

@@ -1,0 +1,121 @@
+"""Per-step measurements of the hot path on one GPU.
+
+    python tools/bench_steps.py [--out profiles/r01_steps.json]
+
+a2  attention kernel: TFLOP/s per config (C2, C2 causal, C3@P=1, C4@P=1, C5@P=1)
+    and per kernel variant, CUDA-event timed on the launch stream
+a4  LSE combine kernel: HBM GB/s (12 B/elem + 12 B/row) at C4 P=8 shard size
+a1+a2+a4 through the single-GPU ring emulation (P = 2, 4, 8) at C3 size:
+    the per-rank compute of the real ring without NCCL (the exchange step,
+    a3, needs >1 GPU and is not measurable here)
+Each line also records the SM clock seen during the run.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+from paper_2302_06218_b200 import dmha  # noqa: E402
+
+PEAKS = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {
+    "hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def time_cuda(fn, iters=5, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def attn_flops(L, D, H, causal):
+    f = 4.0 * L * L * D * H
+    return f / 2 if causal else f
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "steps.json"))
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    res = {"gpu": torch.cuda.get_device_name(0), "peaks": PEAKS, "a2_attention": [], "a4_combine": [],
+           "ring_emulated": []}
+    dmha.init(1, 0, None, 0, "bf16", "contiguous")
+    configs = [("C2", 16384, 64, 8, False), ("C2c", 16384, 64, 8, True), ("C3@P1", 131072, 128, 8, False),
+               ("C4@P1", 262144, 128, 16, False), ("C5@P1", 1048576, 64, 16, True)]
+    if args.quick:
+        configs = configs[:3]
+    for name, L, D, H, causal in configs:
+        q, k, v = (torch.randn(L, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
+        out = torch.empty_like(q)
+        lse = torch.empty(H, L, device="cuda")
+        for kern in ("pingpong", "cluster", "pair"):
+            if kern == "pair" and D != 128:
+                continue
+            os.environ["DMHA_KERNEL"] = kern
+            iters = 2 if L >= 262144 else 10
+            ms = time_cuda(lambda: dmha.forward(q, k, v, L, causal, out, lse), iters=iters, warmup=2)
+            tf = attn_flops(L, D, H, causal) / ms / 1e9
+            res["a2_attention"].append({"config": name, "kernel": kern, "L": L, "D": D, "H": H, "causal": causal,
+                                        "ms": ms, "tflops": tf,
+                                        "frac_sustained": tf / PEAKS["bf16_tflops_sustained"],
+                                        "frac_burst": tf / PEAKS["bf16_tflops"], "frac_datasheet": tf / 2250.0})
+            print(json.dumps(res["a2_attention"][-1]), flush=True)
+        os.environ.pop("DMHA_KERNEL", None)
+        del q, k, v, out, lse
+        torch.cuda.empty_cache()
+
+    # a4: combine kernel at C4 P=8 shard size (L_loc = 32768, H = 16, D = 128)
+    for (Lq, H, D) in ((32768, 16, 128), (131072, 16, 64)):
+        oa, op = (torch.randn(Lq, H, D, device="cuda") for _ in range(2))
+        la, lp = (torch.randn(H, Lq, device="cuda") for _ in range(2))
+        out = torch.empty(Lq, H, D, device="cuda", dtype=torch.bfloat16)
+        lo = torch.empty(H, Lq, device="cuda")
+        ms = time_cuda(lambda: dmha.lse_combine(oa, la, op, lp, final=False), iters=20)
+        by = 12.0 * Lq * H * D + 12.0 * Lq * H
+        ms_f = time_cuda(lambda: dmha.lse_combine(oa, la, op, lp, out, lo, final=True), iters=20)
+        by_f = 10.0 * Lq * H * D + 12.0 * Lq * H
+        rec = {"Lq": Lq, "H": H, "D": D, "ms_accumulate": ms, "gbs_accumulate": by / ms / 1e6,
+               "ms_final_bf16": ms_f, "gbs_final_bf16": by_f / ms_f / 1e6, "hbm_peak_gbs": PEAKS["hbm_gbs"]}
+        rec["frac_accumulate"] = rec["gbs_accumulate"] / PEAKS["hbm_gbs"]
+        res["a4_combine"].append(rec)
+        print(json.dumps(rec), flush=True)
+        del oa, op, la, lp, out, lo
+
+    # whole per-rank ring compute through the emulation (C3 size, P = 2, 4, 8)
+    L, D, H = 131072, 128, 8
+    for P in (2, 4, 8):
+        for layout, causal in (("contiguous", False), ("zigzag", True)):
+            Ll = L // P
+            q, k, v = (torch.randn(P, Ll, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
+            out = torch.empty_like(q)
+            lse = torch.empty(P, H, Ll, device="cuda")
+            ms = time_cuda(lambda: dmha.forward_emulated(P, layout, q, k, v, L, causal, out, lse), iters=3, warmup=1)
+            tf = attn_flops(L, D, H, causal) / ms / 1e9  # all P ranks' work, serialised on one GPU
+            rec = {"P": P, "layout": layout, "causal": causal, "L": L, "D": D, "H": H,
+                   "ms_all_ranks_serial": ms, "tflops_serial": tf,
+                   "projected_ms_per_rank_if_perfectly_parallel": ms / P}
+            res["ring_emulated"].append(rec)
+            print(json.dumps(rec), flush=True)
+            del q, k, v, out, lse
+            torch.cuda.empty_cache()
+    dmha.finalize()
+    Path(args.out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
