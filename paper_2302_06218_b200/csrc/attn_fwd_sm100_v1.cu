@@ -43,6 +43,7 @@
 #include "ptx_sm100.cuh"
 
 namespace dmha {
+extern unsigned long long* g_trace;
 namespace {
 
 constexpr int kBM = 128;          // query rows per tile (MMA M)
@@ -76,7 +77,17 @@ struct Params {
   float* lse;
   int out_mode;
   int n_mblk;
+  unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
+
+// Timeline trace (measurement hook, same buffer layout as the other variants:
+// [cta < 4][event < 9][tile < 64] clock64 stamps, head 0 only).  Events:
+//  0/2: softmax of Q tile 0/1 saw S(j)   1/3: Q tile 0/1 arrive P(j) ready
+//  4/5: MMA thread saw P0(j)/P1(j) ready   6: MMA thread issued S1(j)
+__device__ __forceinline__ void trace_stamp(const Params& p, int ev, int j) {
+  if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < 4 && j < 64)
+    p.trace[(blockIdx.x * 9 + ev) * 64 + j] = clock64();
+}
 
 __device__ __forceinline__ int64_t pos_of(const PosMap& m, int64_t i) {
   return i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
@@ -232,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
         ptx::mbar_wait(&p_ready[0], ppar);
+        trace_stamp(p, 4, j - 1);
         ptx::tc_fence_after();
         pv(0, slotV, j > 1);
         if (more) {
@@ -241,12 +253,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mma_commit(&o_final[0]);
         }
         ptx::mbar_wait(&p_ready[1], ppar);
+        trace_stamp(p, 5, j - 1);
         ptx::tc_fence_after();
         pv(1, slotV, j > 1);
         ptx::mma_commit(&kv_empty[slotV]);
         if (more) {
           qk(1, slotK2);
           ptx::mma_commit(&s_full[1]);
+          trace_stamp(p, 6, j);
           ptx::mma_commit(&kv_empty[slotK2]);
         } else {
           ptx::mma_commit(&o_final[1]);
@@ -272,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float l_run = 0.f;
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(&s_full[g], static_cast<uint32_t>(j & 1));
+      if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g, j);
       ptx::tc_fence_after();
       float s[128];
 #pragma unroll
@@ -337,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
+      if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
       ptx::mbar_arrive(&p_ready[g]);
     }
     if (nkv > 0) {
@@ -458,6 +474,7 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   p.lse = a.lse;
   p.out_mode = a.out_mode;
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
+  p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H);
   attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
