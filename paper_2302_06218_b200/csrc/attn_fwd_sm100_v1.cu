@@ -38,9 +38,11 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx_sm100.cuh"
+#include "softmax_sm100.cuh"
 
 namespace dmha {
 extern unsigned long long* g_trace;
@@ -118,12 +120,15 @@ __device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
   return static_cast<int>((lim + kBN - 1) / kBN);
 }
 
-template <int D>
+template <int D, int kEmu>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const Params p) {
   using C = Cfg<D>;
+  // D = 64: separate P buffers (TMEM has room) decouple S_g(j+1) from PV_g(j).
+  constexpr bool kSepP = (D == 64);
+  constexpr uint32_t kPCol = 256 + 64;  // P_g at kPCol + 128 g (D = 64 only)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -136,7 +141,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_full = kv_empty + C::kStages;   // [2]
   uint64_t* p_ready = s_full + 2;             // [2]
   uint64_t* o_final = p_ready + 2;            // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
+  // D = 64 only (separate P buffers): softmax loaded S_g / PV_g complete.
+  uint64_t* s_free = o_final + 2;             // [2]
+  uint64_t* pv_done = s_free + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -157,6 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&s_full[g], 1);
       ptx::mbar_init(&p_ready[g], kBM);
       ptx::mbar_init(&o_final[g], 1);
+      ptx::mbar_init(&s_free[g], kBM);
+      ptx::mbar_init(&pv_done[g], 1);
     }
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_q);
@@ -206,6 +216,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                            ptx::smem_desc_sw128(b0 + off, 16, 1024), C::kIdescQK, kk > 0);
         }
       };
+      // D = 64: P_g lives at columns [320 + 128g, 384 + 128g) (the unused half
+      // of O_g's 128-column slot).
+      auto pv_sep = [&](int g, int slot, bool acc) {
+        const uint32_t b0 = skv + slot * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          ptx::mma_bf16_ts(tmem + 256 + g * 128, tmem + kPCol + g * 128 + kk * 8,
+                           ptx::smem_desc_sw128(b0 + kk * 16 * 128, C::kPanelBytes, 1024),
+                           C::kIdescPV, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
       auto pv = [&](int g, int slot, bool acc) {
         const uint32_t b0 = skv + slot * C::kTileBytes;
 #pragma unroll
@@ -215,6 +236,50 @@ __global__ void __launch_bounds__(kThreads, 1)
                            C::kIdescPV, (acc || kk > 0) ? 1u : 0u);
         }
       };
+      if constexpr (kSepP) {
+        // D = 64: P_g has its own TMEM columns, so S_g(j) only waits for the
+        // softmax to have LOADED S_g(j-1) (s_free) and runs on the tensor core
+        // during that softmax's exponentials; PV_g(j-1) follows when P is ready.
+        // K/V ring item i: K_t = item 2t, V_t = item 2t+1 (load order).
+        auto slot_of = [](int item) { return item % C::kStages; };
+        auto par_of = [](int item) { return static_cast<uint32_t>((item / C::kStages) & 1); };
+        ptx::mbar_wait(q_full, 0);
+        ptx::mbar_wait(&kv_full[slot_of(0)], par_of(0));
+        ptx::tc_fence_after();
+        qk(0, slot_of(0));
+        ptx::mma_commit(&s_full[0]);
+        qk(1, slot_of(0));
+        ptx::mma_commit(&s_full[1]);
+        ptx::mma_commit(&kv_empty[slot_of(0)]);
+        for (int j = 1; j <= nkv; ++j) {
+          const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
+          if (j < nkv) {  // S_g(j): needs K_j and S_g(j-1) consumed
+            const int ik = 2 * j;
+            ptx::mbar_wait(&kv_full[slot_of(ik)], par_of(ik));
+            ptx::mbar_wait(&s_free[0], ppar);
+            ptx::tc_fence_after();
+            qk(0, slot_of(ik));
+            ptx::mma_commit(&s_full[0]);
+            ptx::mbar_wait(&s_free[1], ppar);
+            ptx::tc_fence_after();
+            qk(1, slot_of(ik));
+            ptx::mma_commit(&s_full[1]);
+            trace_stamp(p, 6, j);
+            ptx::mma_commit(&kv_empty[slot_of(ik)]);
+          }
+          const int iv = 2 * (j - 1) + 1;  // V_{j-1}
+          ptx::mbar_wait(&kv_full[slot_of(iv)], par_of(iv));
+          for (int g = 0; g < 2; ++g) {
+            ptx::mbar_wait(&p_ready[g], ppar);
+            trace_stamp(p, 4 + g, j - 1);
+            ptx::tc_fence_after();
+            pv_sep(g, slot_of(iv), j > 1);
+            ptx::mma_commit(&pv_done[g]);
+            if (j == nkv) ptx::mma_commit(&o_final[g]);
+          }
+          ptx::mma_commit(&kv_empty[slot_of(iv)]);
+        }
+      } else {
       int stage = 0;
       uint32_t phase = 0;
       auto advance = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
@@ -267,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+      }
     __syncwarp();
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax
@@ -293,22 +359,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < 4; ++c)
         ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
       ptx::tmem_wait_ld();
+      if (g == 0 && threadIdx.x == 0) trace_stamp(p, 7, j);
+      if constexpr (kSepP) {  // S_g is in registers: the tensor core may overwrite it
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&s_free[g]);
+      }
 
       int64_t nv64 = klim - static_cast<int64_t>(j) * kBN;
       const int nvalid = nv64 < 0 ? 0 : (nv64 > kBN ? kBN : static_cast<int>(nv64));
-      if (!__all_sync(0xffffffffu, nvalid >= kBN)) {
+      const bool masked = !__all_sync(0xffffffffu, nvalid >= kBN);
+      if (masked) {
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
-      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
-#pragma unroll
-      for (int c = 4; c < 128; c += 4) {
-        mx0 = fmaxf(mx0, s[c]);
-        mx1 = fmaxf(mx1, s[c + 1]);
-        mx2 = fmaxf(mx2, s[c + 2]);
-        mx3 = fmaxf(mx3, s[c + 3]);
-      }
-      const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const float mt = sm::row_max128(s) * sl2;
       const bool need = mt > m_run + kRescaleThreshold;
       const bool warp_rescale = __any_sync(0xffffffffu, need);
       float alpha = 1.f;
@@ -318,27 +382,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run *= alpha;
         m_run = m_new;
       }
-      // P = exp2(S*scale*log2e - m) -> bf16, written over the first 64 columns
-      // of S in 16-column chunks so the fp32 scores die as P is produced.
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float sum0 = 0.f, sum1 = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], sl2, -m_use));
-          const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], sl2, -m_use));
-          sum0 += e0;
-          sum1 += e1;
-          __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
-          pk[e] = *reinterpret_cast<uint32_t*>(&b);
+      if constexpr (kSepP) {
+        // P_g(j) and the O_g rescale need PV_g(j-1) finished (usually long done:
+        // it was issued when P_g(j-1) was ready).
+        if (j > 0) {
+          ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
+          ptx::tc_fence_after();
         }
-        ptx::tmem_st16(tS + c * 16, pk);
       }
-      l_run += sum0 + sum1;
-      // O_g holds PV_g(j-1) (complete: covered by the S_g(j) commit) and PV_g(j)
-      // is not issued before p_ready, so O can be rescaled in place here.
+      // P = exp2(S*scale*log2e - m) -> bf16, written over the first 64 columns
+      // of S (D = 64: into P_g) in 16-column chunks so the fp32 scores die as P
+      // is produced.
+      if (g == 0 && threadIdx.x == 0) trace_stamp(p, 8, j);
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      const uint32_t tP = kSepP ? (tmem + lane_addr + kPCol + g * 128) : tS;
+      // Unmasked tiles send kEmu of every 8 column pairs to the FMA-pipe
+      // polynomial; masked tiles (-inf entries, exact zeros needed) use MUFU only.
+      if (masked)
+        l_run += sm::exp_tile<0>(s, sl2, m_use, tP);
+      else
+        l_run += sm::exp_tile<kEmu>(s, sl2, m_use, tP);
+      // O_g holds PV_g(j-1) (complete: covered by the S_g(j) commit, or by the
+      // pv_done wait when D = 64) and PV_g(j) is not issued before p_ready, so
+      // O can be rescaled in place here.
       if (warp_rescale && j > 0) {
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
@@ -447,8 +513,8 @@ bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
   return r == CUDA_SUCCESS;
 }
 
-template <int D>
-cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
+template <int D, int E>
+cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   using C = Cfg<D>;
   CUtensorMap tq, tk, tv;
   if (!make_map(&tq, a.q, a.Lq, a.H, D) || !make_map(&tk, a.k, a.Lk, a.H, D) ||
@@ -456,7 +522,7 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -476,8 +542,24 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H);
-  attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  attn_fwd_sm100_kernel<D, E><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
+}
+
+
+// DMHA_EMU = pairs (of every 8) of score columns on the FMA-pipe exp2
+// (measurement knob; default 0).
+template <int D>
+cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
+  int emu = 0;
+  if (const char* e = std::getenv("DMHA_EMU")) emu = std::atoi(e);
+  switch (emu) {
+    case 1: return launch_de<D, 1>(a, stream);
+    case 2: return launch_de<D, 2>(a, stream);
+    case 3: return launch_de<D, 3>(a, stream);
+    case 4: return launch_de<D, 4>(a, stream);
+    default: return launch_de<D, 0>(a, stream);
+  }
 }
 
 }  // namespace

@@ -1,0 +1,93 @@
+// softmax_sm100.cuh — exponential helpers shared by the attention kernels:
+// P = exp2(S*scale*log2e - m) for one 128-column score row per thread, on
+// MUFU.EX2 or (for EMU of every 8 column pairs) on the FMA pipe, packed to bf16
+// and stored to TMEM.
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "ptx_sm100.cuh"
+
+namespace dmha {
+namespace sm {
+
+// 2^x for a pair on MUFU.EX2.
+__device__ __forceinline__ float2 exp2_mufu2(float2 x) {
+  return make_float2(ptx::ex2_approx(x.x), ptx::ex2_approx(x.y));
+}
+
+// 2^x for a pair on the FMA pipe (FADD2/FFMA2 + 2 ALU ops per element):
+// n = round(x) via the 1.5*2^23 magic add, f = x - n in [-0.5, 0.5],
+// 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5, below the
+// 2^-9 bf16 rounding P gets anyway), exponent added as (n << 23).
+// x is clamped at -126 so the exponent cannot wrap (only used on unmasked
+// tiles, whose entries are finite).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+  float2 p = __ffma2_rn(f, make_float2(0.055171459913253784f, 0.055171459913253784f),
+                        make_float2(0.2426108568906784f, 0.2426108568906784f));
+  p = __ffma2_rn(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
+  p = __ffma2_rn(p, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
+  const uint32_t rx = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+  const uint32_t ry = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+  return make_float2(__uint_as_float(rx), __uint_as_float(ry));
+}
+
+// P = exp2(S*scale*log2e - m) for one 128-column score row, packed to bf16 and
+// written over the first 64 TMEM columns of the S buffer (16-column chunks, so
+// the fp32 scores die as P is produced).  Returns the fp32 sum of P.
+// EMU of every 8 column pairs use exp2_poly2 (FMA pipe), the rest MUFU.
+template <int EMU>
+__device__ __forceinline__ float exp_tile(float (&s)[128], float sl2, float m_use, uint32_t tP) {
+  const float2 sc2 = make_float2(sl2, sl2);
+  const float2 nm2 = make_float2(-m_use, -m_use);
+  float2 sum_a = make_float2(0.f, 0.f), sum_b = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      // x = S*scale*log2e - m on the packed FP32x2 pipe (FFMA2)
+      const float2 x = __ffma2_rn(make_float2(s[32 * c + 2 * e], s[32 * c + 2 * e + 1]), sc2, nm2);
+      const float2 pe = (((c * 16 + e) & 7) < EMU) ? exp2_poly2(x) : exp2_mufu2(x);
+      if (e & 1)
+        sum_b = __fadd2_rn(sum_b, pe);
+      else
+        sum_a = __fadd2_rn(sum_a, pe);
+      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
+      pk[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    ptx::tmem_st16(tP + c * 16, pk);
+  }
+  return (sum_a.x + sum_a.y) + (sum_b.x + sum_b.y);
+}
+
+// Row max of 128 scores as a shallow tree: 16 independent 3-input max chains
+// of depth 4, then a 3-level tree (instead of 4 serial chains of depth 32).
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  return fmaxf(fmaxf(a, b), c);  // ptxas fuses to FMNMX3
+}
+__device__ __forceinline__ float row_max128(const float (&s)[128]) {
+  float m[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = fmax3(s[i], s[16 + i], s[32 + i]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = fmax3(m[i], s[48 + i], s[64 + i]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = fmax3(m[i], s[80 + i], s[96 + i]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = fmaxf(m[i], s[112 + i]);
+  float t[6];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) t[i] = fmax3(m[3 * i], m[3 * i + 1], m[3 * i + 2]);
+  t[5] = m[15];
+  return fmaxf(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]));
+}
+
+}  // namespace sm
+}  // namespace dmha

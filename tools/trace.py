@@ -30,5 +30,9 @@ for c in range(2):
     sm0 = np.mean([tc[1][j] - tc[0][j] for j in js]); sm1 = np.mean([tc[3][j] - tc[2][j] for j in js])
     w0 = np.mean([tc[0][j + 1] - tc[1][j] for j in js]); w1 = np.mean([tc[2][j + 1] - tc[3][j] for j in js])
     lat0 = np.mean([tc[4][j] - max(tc[1][j], tc[3][j]) for j in js])
+    if t[c][7][10] and t[c][8][10]:
+        ld = np.mean([tc[7][j] - tc[0][j] for j in js]); mx = np.mean([tc[8][j] - tc[7][j] for j in js])
+        ex = np.mean([tc[1][j] - tc[8][j] for j in js])
+        print(f"  WG0 per tile: S load {ld:.0f}  max+decision {mx:.0f}  exp+store+arrive {ex:.0f}")
     print(f"  period/tile {per:.0f}  softmax WG0 {sm0:.0f}  WG1 {sm1:.0f}  wait-S WG0 {w0:.0f}  WG1 {w1:.0f}  P->mma-sees {lat0:.0f}")
 dmha.finalize()
