@@ -188,7 +188,9 @@ def run_reference(args, w):
 
 def config_of(args, w):
     return {"workload": w["desc"], "L": w["L"], "D": w["D"], "H": w["H"], "causal": w["causal"],
-            "layout": w["layout"], "batch": 1, "parallelism": f"seq-ring-cp{args.gpus}",
+            "layout": w["layout"], "batch": 1,
+            "parallelism": (f"seq-ring-cp{args.gpus}" if getattr(args, "exchange", "ring") == "ring"
+                            else f"seq-a2a-headpar{args.gpus}"),
             "l2": "inputs larger than L2 (q,k,v each >= 126 MB per rank)"
             if w["L"] // args.gpus * w["H"] * w["D"] * 2 > 126e6 else
             "L2 flushed (256 MB write) between timed steps"}
@@ -242,8 +244,9 @@ def run_ours(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    fwd = dmha.forward if args.exchange == "ring" else dmha.forward_headpar
     for _ in range(args.warmup):
-        dmha.forward(q, k, v, L, w["causal"], out, lse)
+        fwd(q, k, v, L, w["causal"], out, lse)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -258,7 +261,7 @@ def run_ours(args, w):
             if flush is not None:
                 flush.fill_(i & 0xFF)
             evs[i][0].record(stream)
-            dmha.forward(q, k, v, L, w["causal"], out, lse)
+            fwd(q, k, v, L, w["causal"], out, lse)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -360,6 +363,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--exchange", default="ring", choices=["ring", "headpar"],
+                    help="ring (north_star, default) or the paper's all-to-all head-parallel exchange")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

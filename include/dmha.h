@@ -130,6 +130,22 @@ int dmha_forward_emulated(int world_size, int layout, const void *q, const void 
                           const void *v, void *out, float *lse, int64_t L, int D, int H,
                           int causal);
 
+/* NEXT-1 — the paper's own distributed algorithm (§10.4):
+ * all-to-all from sequence-parallel to head-parallel (each rank receives all
+ * L rows of H/P heads), full-L attention per head on each rank
+ * (P:674), all-to-all back to sequence-parallel.  Same arguments,
+ * layouts and result as dmha_forward; requires H % world_size == 0.  The two
+ * exchanges are blocking steps on the compute stream (as in the paper); the
+ * ring (dmha_forward) overlaps its exchange instead. */
+int dmha_forward_headpar(const void *q, const void *k, const void *v, void *out, float *lse,
+                         int64_t L, int D, int H, int causal);
+
+/* Single-GPU emulation of dmha_forward_headpar at world size P (buffers as in
+ * dmha_forward_emulated); the all-to-alls become device copies. */
+int dmha_forward_headpar_emulated(int world_size, int layout, const void *q, const void *k,
+                                  const void *v, void *out, float *lse, int64_t L, int D, int H,
+                                  int causal);
+
 /* Device bytes the library will hold per rank for (L, D, H) at the initialised
  * world size and dtype (ring buffers + fp32 accumulators + staging excluded). */
 int dmha_workspace_bytes(int64_t L, int D, int H, size_t *bytes_out);

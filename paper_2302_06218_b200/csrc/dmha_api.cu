@@ -72,6 +72,9 @@ struct State {
   float* lse_acc = nullptr;
   float* lse_part = nullptr;
   size_t kv_bytes = 0, acc_elems = 0, lse_elems = 0;
+  // head-parallel exchange workspace (dmha_forward_headpar*)
+  void* hp = nullptr;
+  size_t hp_bytes = 0;
   // host-path staging
   void* st_qkv = nullptr;  // q, k, v back to back
   void* st_out = nullptr;
@@ -152,7 +155,7 @@ void free_ptr(float*& p) {
 
 void update_ws_stat() {
   g.stats.workspace_bytes = 2 * g.kv_bytes + 2 * g.acc_elems * 4 + 2 * g.lse_elems * 4 +
-                            g.st_bytes + g.st_lse_elems * 4;
+                            g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes;
 }
 
 int alloc_or_oom(void** p, size_t bytes, const char* what) {
@@ -371,6 +374,94 @@ int poll_nccl() {
   return DMHA_OK;
 }
 
+// ---------------------------------------------------------------- head-parallel
+// The paper's distributed MHA (§10.4):
+//   pack -> all-to-all (seq-parallel -> head-parallel) -> unpack to global
+//   order -> full-L attention for H/P heads -> pack -> all-to-all back ->
+//   unpack.  `exchange(bytes_per_peer, send, recv)` moves block d of `send` to
+// rank d and block s from rank s into `recv` (NCCL or the emulation).
+struct HpLayout {
+  size_t qkv_blk, out_blk, lse_blk;  // bytes per peer block
+  size_t send1, recv1, xq, xk, xv, outg, lseg, send2, recv2, send_lse, total;
+};
+
+HpLayout hp_layout(int P, int64_t Lloc, int H, int D, size_t e) {
+  HpLayout y{};
+  const size_t rows_heads = static_cast<size_t>(Lloc) * (H / P);
+  y.qkv_blk = 3 * rows_heads * D * e;
+  y.out_blk = rows_heads * D * e;
+  y.lse_blk = rows_heads * 4;
+  size_t off = 0;
+  auto take = [&](size_t n) { size_t o = off; off += (n + 255) & ~size_t(255); return o; };
+  y.send1 = take(P * y.qkv_blk);
+  y.recv1 = take(P * y.qkv_blk);
+  y.xq = take(P * y.out_blk);
+  y.xk = take(P * y.out_blk);
+  y.xv = take(P * y.out_blk);
+  y.outg = take(P * y.out_blk);
+  y.lseg = take(P * y.lse_blk);
+  y.send2 = take(P * y.out_blk);
+  y.recv2 = take(P * y.out_blk);
+  y.send_lse = take(P * y.lse_blk);
+  y.total = off;
+  return y;
+}
+
+int ensure_hp(size_t bytes) {
+  if (bytes <= g.hp_bytes) return DMHA_OK;
+  free_ptr(g.hp);
+  g.hp_bytes = 0;
+  if (int rc = alloc_or_oom(&g.hp, bytes, "head-parallel workspace")) return rc;
+  g.hp_bytes = bytes;
+  update_ws_stat();
+  return DMHA_OK;
+}
+
+#define CK_LAUNCH(expr)                                                                   \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) return fail(DMHA_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    g.stats.kernel_launches++;                                                            \
+  } while (0)
+
+// One rank's head-parallel forward; `ws` is this rank's workspace (layout y).
+template <typename Ex1, typename Ex2>
+int headpar_rank(int P, int r, int layout, const void* q, const void* k, const void* v,
+                 void* out, float* lse, int64_t L, int D, int H, int causal, char* ws,
+                 const HpLayout& y, Ex1&& exchange_qkv, Ex2&& exchange_out,
+                 bool do_exchange_out_now) {
+  (void)r;
+  const int64_t Lloc = L / P;
+  const int e = static_cast<int>(elem_bytes(g.dtype));
+  const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
+  CK_LAUNCH(dmha::launch_headpar_pack_qkv(q, k, v, ws + y.send1, geo, e, g.stream));
+  if (int rc = exchange_qkv()) return rc;
+  CK_LAUNCH(dmha::launch_headpar_unpack_qkv(ws + y.recv1, ws + y.xq, ws + y.xk, ws + y.xv, geo,
+                                            e, g.stream));
+  const dmha::PosMap full{0, L, L};
+  if (int rc = run_local(ws + y.xq, ws + y.xk, ws + y.xv, ws + y.outg,
+                         reinterpret_cast<float*>(ws + y.lseg), L, L, D, H / P, causal, full, full,
+                         dmha::OUT_FINAL))
+    return rc;
+  CK_LAUNCH(dmha::launch_headpar_pack_out(ws + y.outg, ws + y.send2,
+                                          reinterpret_cast<const float*>(ws + y.lseg),
+                                          reinterpret_cast<float*>(ws + y.send_lse), geo, e,
+                                          g.stream));
+  if (do_exchange_out_now) {
+    if (int rc = exchange_out()) return rc;
+    CK_LAUNCH(dmha::launch_headpar_unpack_out(ws + y.recv2, out, geo, e, g.stream));
+  }
+  (void)lse;
+  return DMHA_OK;
+}
+
+int validate_headpar(int P, int64_t L, int H) {
+  if (P < 1 || H % P != 0)
+    return fail(DMHA_ERR_INVALID, "dmha headpar: H=%d must be divisible by the world size %d", H, P);
+  (void)L;
+  return DMHA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -451,6 +542,7 @@ int dmha_finalize(void) {
   free_ptr(g.st_qkv);
   free_ptr(g.st_out);
   free_ptr(g.st_lse);
+  free_ptr(g.hp);
   resolve_profiles();
   for (cudaEvent_t e : g.pool) cudaEventDestroy(e);
   g.pool.clear();
@@ -641,6 +733,119 @@ int dmha_forward_emulated(int world_size, int layout, const void* q, const void*
       if (s < P - 1) g.stats.bytes_sent += 2 * blk;
       g.stats.ring_steps++;
     }
+  }
+  g.stats.forwards++;
+  return DMHA_OK;
+}
+
+int dmha_forward_headpar(const void* q, const void* k, const void* v, void* out, float* lse,
+                         int64_t L, int D, int H, int causal) {
+  if (int rc = check_state()) return rc;
+  if (int rc = validate(q, k, v, out, lse, L, D, H, g.world, g.layout)) return rc;
+  if (int rc = validate_headpar(g.world, L, H)) return rc;
+  if (int rc = poll_nccl()) return rc;
+  const int P = g.world, r = g.rank;
+  causal = causal ? 1 : 0;
+  if (P == 1) return dmha_forward(q, k, v, out, lse, L, D, H, causal);
+  const int64_t Lloc = L / P;
+  const HpLayout y = hp_layout(P, Lloc, H, D, elem_bytes(g.dtype));
+  if (int rc = ensure_hp(y.total)) return rc;
+  char* ws = static_cast<char*>(g.hp);
+  // Both all-to-alls run on the compute stream: the paper's shuffles are
+  // blocking steps between the projections and the per-head softmax.
+  auto a2a = [&](size_t send_off, size_t recv_off, size_t blk) -> int {
+    CK_NCCL(ncclGroupStart());
+    for (int d = 0; d < P; ++d) {
+      CK_NCCL(ncclSend(ws + send_off + d * blk, blk, ncclChar, d, g.nccl, g.stream));
+      CK_NCCL(ncclRecv(ws + recv_off + d * blk, blk, ncclChar, d, g.nccl, g.stream));
+    }
+    CK_NCCL(ncclGroupEnd());
+    g.stats.bytes_sent += (P - 1) * blk;
+    return DMHA_OK;
+  };
+  auto ex1 = [&]() -> int { return a2a(y.send1, y.recv1, y.qkv_blk); };
+  auto ex2 = [&]() -> int {
+    if (int rc = a2a(y.send2, y.recv2, y.out_blk)) return rc;
+    // lse blocks land directly in the caller's [H, Lloc] lse (block s = heads of s)
+    CK_NCCL(ncclGroupStart());
+    for (int d = 0; d < P; ++d) {
+      CK_NCCL(ncclSend(ws + y.send_lse + d * y.lse_blk, y.lse_blk, ncclChar, d, g.nccl, g.stream));
+      CK_NCCL(ncclRecv(reinterpret_cast<char*>(lse) + d * y.lse_blk, y.lse_blk, ncclChar, d,
+                       g.nccl, g.stream));
+    }
+    CK_NCCL(ncclGroupEnd());
+    g.stats.bytes_sent += (P - 1) * y.lse_blk;
+    return DMHA_OK;
+  };
+  int rc = headpar_rank(P, r, g.layout, q, k, v, out, lse, L, D, H, causal, ws, y, ex1, ex2, true);
+  if (rc) return rc;
+  g.stats.forwards++;
+  return DMHA_OK;
+}
+
+int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, const void* k,
+                                  const void* v, void* out, float* lse, int64_t L, int D, int H,
+                                  int causal) {
+  if (int rc = check_state()) return rc;
+  if (world_size < 1) return fail(DMHA_ERR_INVALID, "dmha_forward_headpar_emulated: world_size < 1");
+  if (int rc = validate(q, k, v, out, lse, L, D, H, world_size, layout)) return rc;
+  if (int rc = validate_headpar(world_size, L, H)) return rc;
+  const int P = world_size;
+  const int64_t Lloc = L / P;
+  causal = causal ? 1 : 0;
+  const size_t e = elem_bytes(g.dtype);
+  const size_t shard = static_cast<size_t>(Lloc) * H * D * e;
+  const size_t lshard = static_cast<size_t>(Lloc) * H * 4;
+  const HpLayout y = hp_layout(P, Lloc, H, D, e);
+  if (int rc = ensure_hp(P * y.total)) return rc;
+  char* base = static_cast<char*>(g.hp);
+  auto ws_of = [&](int r) { return base + static_cast<size_t>(r) * y.total; };
+  auto nothing = []() -> int { return DMHA_OK; };
+  // Phase 1: every rank packs; the all-to-all is P*P device copies.
+  for (int r = 0; r < P; ++r) {
+    const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
+    CK_LAUNCH(dmha::launch_headpar_pack_qkv(static_cast<const char*>(q) + r * shard,
+                                            static_cast<const char*>(k) + r * shard,
+                                            static_cast<const char*>(v) + r * shard,
+                                            ws_of(r) + y.send1, geo, static_cast<int>(e), g.stream));
+  }
+  for (int s = 0; s < P; ++s)
+    for (int d = 0; d < P; ++d)
+      CK_CUDA(cudaMemcpyAsync(ws_of(d) + y.recv1 + s * y.qkv_blk, ws_of(s) + y.send1 + d * y.qkv_blk,
+                              y.qkv_blk, cudaMemcpyDeviceToDevice, g.stream));
+  g.stats.bytes_sent += static_cast<uint64_t>(P) * (P - 1) * y.qkv_blk;
+  // Phase 2: per rank unpack, attention for its heads, pack (no-op exchanges).
+  for (int r = 0; r < P; ++r) {
+    const int64_t Lg = L;
+    const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
+    char* ws = ws_of(r);
+    CK_LAUNCH(dmha::launch_headpar_unpack_qkv(ws + y.recv1, ws + y.xq, ws + y.xk, ws + y.xv, geo,
+                                              static_cast<int>(e), g.stream));
+    const dmha::PosMap full{0, Lg, Lg};
+    if (int rc = run_local(ws + y.xq, ws + y.xk, ws + y.xv, ws + y.outg,
+                           reinterpret_cast<float*>(ws + y.lseg), Lg, Lg, D, H / P, causal, full,
+                           full, dmha::OUT_FINAL))
+      return rc;
+    CK_LAUNCH(dmha::launch_headpar_pack_out(ws + y.outg, ws + y.send2,
+                                            reinterpret_cast<const float*>(ws + y.lseg),
+                                            reinterpret_cast<float*>(ws + y.send_lse), geo,
+                                            static_cast<int>(e), g.stream));
+  }
+  (void)nothing;
+  // Phase 3: all-to-all back (out blocks and lse blocks), unpack per rank.
+  for (int s = 0; s < P; ++s)
+    for (int d = 0; d < P; ++d) {
+      CK_CUDA(cudaMemcpyAsync(ws_of(d) + y.recv2 + s * y.out_blk, ws_of(s) + y.send2 + d * y.out_blk,
+                              y.out_blk, cudaMemcpyDeviceToDevice, g.stream));
+      CK_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(lse) + d * lshard + s * y.lse_blk,
+                              ws_of(s) + y.send_lse + d * y.lse_blk, y.lse_blk,
+                              cudaMemcpyDeviceToDevice, g.stream));
+    }
+  g.stats.bytes_sent += static_cast<uint64_t>(P) * (P - 1) * (y.out_blk + y.lse_blk);
+  for (int r = 0; r < P; ++r) {
+    const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
+    CK_LAUNCH(dmha::launch_headpar_unpack_out(ws_of(r) + y.recv2, static_cast<char*>(out) + r * shard,
+                                              geo, static_cast<int>(e), g.stream));
   }
   g.stats.forwards++;
   return DMHA_OK;

@@ -43,6 +43,23 @@ cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part
                                int D, int H, int final_step, int out_dtype_bf16,
                                cudaStream_t stream);
 
+// Head-parallel exchange (the paper's all-to-all).
+struct HeadparGeom {
+  int P;         // world size
+  int H, D;      // heads (H % P == 0), per-head dim
+  int64_t Lloc;  // rows per rank
+  int zigzag;    // layout of the sequence shards
+};
+cudaError_t launch_headpar_pack_qkv(const void* q, const void* k, const void* v, void* send,
+                                    const HeadparGeom& g, int elem_bytes, cudaStream_t st);
+cudaError_t launch_headpar_unpack_qkv(const void* recv, void* xq, void* xk, void* xv,
+                                      const HeadparGeom& g, int elem_bytes, cudaStream_t st);
+cudaError_t launch_headpar_pack_out(const void* outg, void* send, const float* lseg,
+                                    float* send_lse, const HeadparGeom& g, int elem_bytes,
+                                    cudaStream_t st);
+cudaError_t launch_headpar_unpack_out(const void* recv, void* out, const HeadparGeom& g,
+                                      int elem_bytes, cudaStream_t st);
+
 // Debug timeline buffer for the bf16 attention kernel (null = off).
 extern unsigned long long* g_trace;
 

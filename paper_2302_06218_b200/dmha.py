@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "dmha_forward", "dmha_forward_host", "dmha_forward_emulated", "dmha_workspace_bytes",
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
     "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
+    "dmha_forward_headpar", "dmha_forward_headpar_emulated",
 )
 
 
@@ -83,6 +84,8 @@ def lib():
             "dmha_set_profiling": [I],
             "dmha_debug_set_trace": [P],
             "dmha_ring_plan_step": [I, I, I, I, I64, ctypes.POINTER(RingPlan)],
+            "dmha_forward_headpar": [P, P, P, P, P, I64, I, I, I],
+            "dmha_forward_headpar_emulated": [I, I, P, P, P, P, P, I64, I, I, I],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -204,6 +207,38 @@ def forward_emulated(world_size: int, layout, q, k, v, L: int, causal: bool = Fa
     set_stream(_cur_stream())
     _check(lib().dmha_forward_emulated(world_size, layout_code(layout), _ptr(q), _ptr(k), _ptr(v),
                                        _ptr(out), _ptr(lse), int(L), D, H, int(bool(causal))))
+    return out, lse
+
+
+def forward_headpar(q, k, v, L: int, causal: bool = False, out=None, lse=None):
+    """The paper's head-parallel algorithm (two all-to-alls); same
+    contract as forward()."""
+    import torch
+    Lloc, H, D = q.shape
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((H, Lloc), dtype=torch.float32, device=q.device)
+    set_stream(_cur_stream())
+    _check(lib().dmha_forward_headpar(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
+                                      int(bool(causal))))
+    return out, lse
+
+
+def forward_headpar_emulated(world_size: int, layout, q, k, v, L: int, causal: bool = False,
+                             out=None, lse=None):
+    """Single-GPU emulation of forward_headpar; q/k/v are [P, L/P, H, D]."""
+    import torch
+    P, Lloc, H, D = q.shape
+    assert P == world_size
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((P, H, Lloc), dtype=torch.float32, device=q.device)
+    set_stream(_cur_stream())
+    _check(lib().dmha_forward_headpar_emulated(world_size, layout_code(layout), _ptr(q), _ptr(k),
+                                               _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
+                                               int(bool(causal))))
     return out, lse
 
 

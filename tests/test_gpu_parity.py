@@ -259,3 +259,32 @@ def test_kernel_variants_ring_partials(lib_bf16, oracle_mod, monkeypatch, kernel
     lg = dmha.unshard([x.T for x in lse.cpu().numpy()], L, "zigzag").T
     ref_o, ref_l = oracle_mod.attention(q, k, v, True)
     assert_parity(og, lg, ref_o, ref_l, "bf16", f"{kernel} ring")
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("layout", ["contiguous", "zigzag"])
+@pytest.mark.parametrize("causal", [False, True])
+def test_headpar_emulated_matches_oracle_and_ring(lib_bf16, oracle_mod, P, layout, causal):
+    """NEXT-1, the paper's own exchange: head-parallel all-to-all
+    path vs the oracle, and vs the ring (two distributions, one result)."""
+    L, H, D = 2048 + 128 * P, 4, 64 if P == 2 else 128
+    q, k, v = inputs.qkv(L, H, D, seed=600 + P)
+    parts = [np.stack([dmha.shard(x, P, r, layout) for r in range(P)]) for x in (q, k, v)]
+    dq, dk, dv = (to_dev(p) for p in parts)
+    out, lse = dmha.forward_headpar_emulated(P, layout, dq, dk, dv, L, causal)
+    torch.cuda.synchronize()
+    og = dmha.unshard(list(out.float().cpu().numpy()), L, layout)
+    lg = dmha.unshard([x.T for x in lse.cpu().numpy()], L, layout).T
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(og, lg, ref_o, ref_l, "bf16", f"headpar P={P} {layout} causal={causal}")
+    ro, rl = dmha.forward_emulated(P, layout, dq, dk, dv, L, causal)
+    torch.cuda.synchronize()
+    ma, rel = metrics(out.float().cpu().numpy(), ro.float().cpu().numpy())
+    assert ma <= 2e-2 and rel <= 5e-3
+
+
+def test_headpar_requires_divisible_heads(lib_bf16):
+    x = torch.zeros((2, 64, 3, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(dmha.DmhaError) as e:
+        dmha.forward_headpar_emulated(2, "contiguous", x, x.clone(), x.clone(), 128, False)
+    assert e.value.code == dmha.ERR_INVALID
