@@ -50,9 +50,15 @@ namespace {
 
 constexpr int kBM = 128;          // query rows per tile (MMA M)
 constexpr int kBN = 128;          // keys per tile (MMA N of QK^T, K of PV)
-constexpr int kThreads = 384;     // 12 warps
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
+// Warp roles: kSm softmax warps (8, or 16 with the split softmax), then the
+// TMA producer, the MMA warp and two idle warps.
+template <bool kSplit>
+struct Roles {
+  static constexpr int kSm = kSplit ? 16 : 8;
+  static constexpr int kProducerWarp = kSm;
+  static constexpr int kMmaWarp = kSm + 1;
+  static constexpr int kThreads = (kSm + 4) * 32;
+};
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
 
 template <int D>
@@ -63,7 +69,8 @@ struct Cfg {
   static constexpr int kStages = (D == 128) ? 4 : 6;        // K/V ring slots
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = 2 * kTileBytes;
-  static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
+  static constexpr int kRedOff = kKVOff + kStages * kTileBytes;  // split softmax: [2][2][2][128] f32 + l [2][2][128]
+  static constexpr int kBarOff = kRedOff + 12 * 128 * 4;
   static constexpr int kSmemBytes = kBarOff + 256 + 1024;   // + barriers + align slack
   static constexpr uint32_t kIdescQK = ptx::make_idesc(1, kBM, kBN, 0, 0);
   static constexpr uint32_t kIdescPV = ptx::make_idesc(1, kBM, D, 0, 1);  // V is MN-major
@@ -120,12 +127,15 @@ __device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
   return static_cast<int>((lim + kBN - 1) / kBN);
 }
 
-template <int D, int kEmu>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int D, int kEmu, bool kSplit>
+__global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const Params p) {
   using C = Cfg<D>;
+  using R = Roles<kSplit>;
+  constexpr int kProducerWarp = R::kProducerWarp;
+  constexpr int kMmaWarp = R::kMmaWarp;
   // D = 64: separate P buffers (TMEM has room) decouple S_g(j+1) from PV_g(j).
   constexpr bool kSepP = (D == 64);
   constexpr uint32_t kPCol = 256 + 64;  // P_g at kPCol + 128 g (D = 64 only)
@@ -163,9 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int g = 0; g < 2; ++g) {
       ptx::mbar_init(&s_full[g], 1);
-      ptx::mbar_init(&p_ready[g], kBM);
+      ptx::mbar_init(&p_ready[g], kSplit ? 2 * kBM : kBM);  // every softmax thread of the Q tile
       ptx::mbar_init(&o_final[g], 1);
-      ptx::mbar_init(&s_free[g], kBM);
+      ptx::mbar_init(&s_free[g], kSplit ? 2 * kBM : kBM);
       ptx::mbar_init(&pv_done[g], 1);
     }
     ptx::fence_mbar_init();
@@ -334,7 +344,137 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
       }
     __syncwarp();
-  } else if (warp < 8) {
+  } else if (kSplit && warp < R::kSm) {
+    // ------------------------------------------------------------ split softmax
+    // Two warpgroups per Q tile: warpgroup (g, h) handles score columns
+    // [64h, 64h+64) of every row of Q tile g, so 8 warps (2 per SMSP) feed
+    // MUFU during a tile's exponentials.  The row max is swapped through
+    // shared memory (slot by tile parity); each half keeps its share of l and
+    // rescales / writes half of O's columns.
+    float* red = reinterpret_cast<float*>(smem + C::kRedOff);  // [parity][g][h][128]
+    float* redl = red + 8 * kBM;                               // [g][h][128]
+    const int wg = warp >> 2;
+    const int g = wg & 1;                     // Q tile
+    const int h = wg >> 1;                    // column half
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int64_t row = m0 + g * kBM + r;
+    const bool row_ok = row < p.Lq;
+    const int64_t qp = pos_of(p.qmap, row_ok ? row : p.Lq - 1);
+    const int64_t klim = key_limit(p, qp);
+    const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + g * kBN;
+    const uint32_t tO = tmem + lane_addr + 256 + g * 128 + h * (D / 2);
+    const uint32_t tP = (kSepP ? (tmem + lane_addr + kPCol + g * 128) : tS) + h * 32;
+    const float sl2 = p.scale_log2;
+    float m_run = -INFINITY;
+    float l_run = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      ptx::mbar_wait(&s_full[g], static_cast<uint32_t>(j & 1));
+      if (h == 0 && threadIdx.x % 128 == 0) trace_stamp(p, 2 * g, j);
+      ptx::tc_fence_after();
+      float s[64];
+      ptx::tmem_ld32(tS + h * 64, *reinterpret_cast<float(*)[32]>(&s[0]));
+      ptx::tmem_ld32(tS + h * 64 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+      ptx::tmem_wait_ld();
+      if constexpr (kSepP) {
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&s_free[g]);
+      }
+      const int64_t tile_lim = klim - static_cast<int64_t>(j) * kBN;
+      const bool masked = !__all_sync(0xffffffffu, tile_lim >= kBN);  // same in both halves
+      if (masked) {
+        const int64_t nv64 = tile_lim - h * 64;
+        const int nvalid = nv64 < 0 ? 0 : (nv64 > 64 ? 64 : static_cast<int>(nv64));
+#pragma unroll
+        for (int c = 0; c < 64; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
+      }
+      const float pmax = sm::row_max64(s);
+      float* red_t = red + ((j & 1) * 2 + g) * 2 * kBM;
+      red_t[h * kBM + r] = pmax;
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+      const float mt = fmaxf(pmax, red_t[(h ^ 1) * kBM + r]) * sl2;
+      const bool need = mt > m_run + kRescaleThreshold;
+      const bool warp_rescale = __any_sync(0xffffffffu, need);  // same in both halves
+      float alpha = 1.f;
+      if (warp_rescale) {
+        const float m_new = fmaxf(m_run, mt);
+        alpha = (m_new == -INFINITY) ? 1.f : ptx::ex2_approx(m_run - m_new);
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      if constexpr (kSepP) {
+        if (j > 0) {
+          ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
+          ptx::tc_fence_after();
+        }
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      l_run += sm::exp_half(s, sl2, m_use, tP);
+      if (warp_rescale && j > 0) {  // this half's D/2 columns of O
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          float o[32];
+          ptx::tmem_ld32(tO + c * 32, o);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] *= alpha;
+          ptx::tmem_st32(tO + c * 32, o);
+        }
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      if (h == 0 && threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
+      ptx::mbar_arrive(&p_ready[g]);
+    }
+    if (nkv > 0) {
+      ptx::mbar_wait(&o_final[g], 0);
+      ptx::tc_fence_after();
+    }
+    redl[(g * 2 + h) * kBM + r] = l_run;
+    asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+    const float l_tot = l_run + redl[(g * 2 + (h ^ 1)) * kBM + r];
+    const bool empty = !(l_tot > 0.f);
+    const float inv_l = empty ? 0.f : 1.f / l_tot;
+    if (row_ok && h == 0)
+      p.lse[static_cast<int64_t>(head) * p.Lq + row] =
+          empty ? -INFINITY : (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
+    const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D) + h * (D / 2);
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      float o[32];
+      if (nkv > 0) {
+        ptx::tmem_ld32(tO + c * 32, o);
+        ptx::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = 0.f;
+      }
+      if (row_ok) {
+        if (p.out_mode == OUT_PARTIAL_F32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dst[e] = make_float4(o[4 * e] * inv_l, o[4 * e + 1] * inv_l, o[4 * e + 2] * inv_l,
+                                 o[4 * e + 3] * inv_l);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
+                                                c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t wd[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(o[8 * e + 2 * t] * inv_l,
+                                                       o[8 * e + 2 * t + 1] * inv_l);
+              wd[t] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[e] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+          }
+        }
+      }
+    }
+  } else if (!kSplit && warp < 8) {
     // ------------------------------------------------------------ softmax
     const int g = warp >> 2;                  // Q tile of this warpgroup
     const int quarter = warp & 3;             // TMEM lane quarter
@@ -372,7 +512,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
-      const float mt = sm::row_max128(s) * sl2;
+      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+#pragma unroll
+      for (int c = 4; c < 128; c += 4) {
+        mx0 = fmaxf(mx0, s[c]);
+        mx1 = fmaxf(mx1, s[c + 1]);
+        mx2 = fmaxf(mx2, s[c + 2]);
+        mx3 = fmaxf(mx3, s[c + 3]);
+      }
+      const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
       const bool need = mt > m_run + kRescaleThreshold;
       const bool warp_rescale = __any_sync(0xffffffffu, need);
       float alpha = 1.f;
@@ -398,10 +546,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tP = kSepP ? (tmem + lane_addr + kPCol + g * 128) : tS;
       // Unmasked tiles send kEmu of every 8 column pairs to the FMA-pipe
       // polynomial; masked tiles (-inf entries, exact zeros needed) use MUFU only.
-      if (masked)
-        l_run += sm::exp_tile<0>(s, sl2, m_use, tP);
-      else
+      if (kEmu == 0 || masked) {
+        // scalar FFMA + MUFU.EX2 (the measured-fastest form on B200)
+        float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], sl2, -m_use));
+            const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], sl2, -m_use));
+            sum0 += e0;
+            sum1 += e1;
+            __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
+            pk[e] = *reinterpret_cast<uint32_t*>(&b);
+          }
+          ptx::tmem_st16(tP + c * 16, pk);
+        }
+        l_run += sum0 + sum1;
+      } else if (kEmu == 8) {
+        l_run += sm::exp_tile_2pass(s, sl2, m_use, tP);
+      } else {
         l_run += sm::exp_tile<kEmu>(s, sl2, m_use, tP);
+      }
       // O_g holds PV_g(j-1) (complete: covered by the S_g(j) commit, or by the
       // pv_done wait when D = 64) and PV_g(j) is not issued before p_ready, so
       // O can be rescaled in place here.
@@ -513,7 +680,7 @@ bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
   return r == CUDA_SUCCESS;
 }
 
-template <int D, int E>
+template <int D, int E, bool S>
 cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   using C = Cfg<D>;
   CUtensorMap tq, tk, tv;
@@ -522,7 +689,7 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E>,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, S>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -542,7 +709,7 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H);
-  attn_fwd_sm100_kernel<D, E><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  attn_fwd_sm100_kernel<D, E, S><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
@@ -553,12 +720,14 @@ template <int D>
 cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   int emu = 0;
   if (const char* e = std::getenv("DMHA_EMU")) emu = std::atoi(e);
+  bool split = false;
+  if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
+  if (split) return launch_de<D, 0, true>(a, stream);
   switch (emu) {
-    case 1: return launch_de<D, 1>(a, stream);
-    case 2: return launch_de<D, 2>(a, stream);
-    case 3: return launch_de<D, 3>(a, stream);
-    case 4: return launch_de<D, 4>(a, stream);
-    default: return launch_de<D, 0>(a, stream);
+    case 1: return launch_de<D, 1, false>(a, stream);
+    case 2: return launch_de<D, 2, false>(a, stream);
+    case 8: return launch_de<D, 8, false>(a, stream);  // two-pass exponentials
+    default: return launch_de<D, 0, false>(a, stream);
   }
 }
 

@@ -67,6 +67,74 @@ __device__ __forceinline__ float exp_tile(float (&s)[128], float sl2, float m_us
   return (sum_a.x + sum_a.y) + (sum_b.x + sum_b.y);
 }
 
+// Same for one half row (64 columns -> 32 P columns at tP).
+__device__ __forceinline__ float exp_half(float (&s)[64], float sl2, float m_use, uint32_t tP) {
+  const float2 sc2 = make_float2(sl2, sl2);
+  const float2 nm2 = make_float2(-m_use, -m_use);
+  float2 sum_a = make_float2(0.f, 0.f), sum_b = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float2 x = __ffma2_rn(make_float2(s[32 * c + 2 * e], s[32 * c + 2 * e + 1]), sc2, nm2);
+      const float2 pe = exp2_mufu2(x);
+      if (e & 1)
+        sum_b = __fadd2_rn(sum_b, pe);
+      else
+        sum_a = __fadd2_rn(sum_a, pe);
+      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
+      pk[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    ptx::tmem_st16(tP + c * 16, pk);
+  }
+  return (sum_a.x + sum_a.y) + (sum_b.x + sum_b.y);
+}
+
+__device__ __forceinline__ float row_max64(const float (&s)[64]) {
+  float m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = fmaxf(fmaxf(s[i], s[8 + i]), s[16 + i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = fmaxf(fmaxf(m[i], s[24 + i]), s[32 + i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = fmaxf(fmaxf(m[i], s[40 + i]), s[48 + i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = fmaxf(m[i], s[56 + i]);
+  const float a = fmaxf(fmaxf(m[0], m[1]), m[2]), b = fmaxf(fmaxf(m[3], m[4]), m[5]);
+  return fmaxf(fmaxf(a, b), fmaxf(m[6], m[7]));
+}
+
+// Two-pass variant: all 128 exponentials first (in place, long independent
+// MUFU streams), then bf16 packing and the TMEM stores.
+__device__ __forceinline__ float exp_tile_2pass(float (&s)[128], float sl2, float m_use,
+                                                uint32_t tP) {
+  const float2 sc2 = make_float2(sl2, sl2);
+  const float2 nm2 = make_float2(-m_use, -m_use);
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+    s[2 * i] = ptx::ex2_approx(x.x);
+    s[2 * i + 1] = ptx::ex2_approx(x.y);
+  }
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                   make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float2 pe = make_float2(s[32 * c + 2 * e], s[32 * c + 2 * e + 1]);
+      acc[e & 3] = __fadd2_rn(acc[e & 3], pe);
+      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
+      pk[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    ptx::tmem_st16(tP + c * 16, pk);
+  }
+  const float2 t = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+  return t.x + t.y;
+}
+
 // Row max of 128 scores as a shallow tree: 16 independent 3-input max chains
 // of depth 4, then a 3-level tree (instead of 4 serial chains of depth 32).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
