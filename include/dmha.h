@@ -140,6 +140,21 @@ int dmha_forward_emulated(int world_size, int layout, const void *q, const void 
 int dmha_forward_headpar(const void *q, const void *k, const void *v, void *out, float *lse,
                          int64_t L, int D, int H, int causal);
 
+/* NEXT-3 — the full distributed MHA layer around the attention:
+ * Q = X W_Q, K = X W_K, V = X W_V with the weights replicated on every rank
+ * and applied to this rank's rows for all heads; the
+ * distributed attention (dmha_forward); Y = concat_h(O) W_0.
+ *  x: DEVICE [L_loc, d_model] bf16 (this rank's rows, layout of dmha_init);
+ *  wq, wk, wv: DEVICE [d_model, H*D] bf16 row-major (head h = columns
+ *  [h*D, (h+1)*D)); wo: DEVICE [H*D, d_model]; y: DEVICE [L_loc, d_model] bf16;
+ *  lse: DEVICE [H, L_loc] fp32 or NULL.  bf16 dtype only; d_model % 8 == 0.
+ * The projections are plain cuBLAS bf16 GEMMs (fp32 accumulate); Q, K, V and
+ * O are kept as bf16 activations in library workspace (reading R17).
+ * Collective like dmha_forward. */
+int dmha_mha_forward(const void *x, const void *wq, const void *wk, const void *wv,
+                     const void *wo, void *y, float *lse, int64_t L, int d_model, int D, int H,
+                     int causal);
+
 /* Single-GPU emulation of dmha_forward_headpar at world size P (buffers as in
  * dmha_forward_emulated); the all-to-alls become device copies. */
 int dmha_forward_headpar_emulated(int world_size, int layout, const void *q, const void *k,

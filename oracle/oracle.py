@@ -165,6 +165,31 @@ def attention_decimal(q, k, v, causal: bool = False, digits: int = 50):
     return out, lse
 
 
+def round_bf16(a):
+    """Round to the nearest bf16 (ties to even) — the storage format of the
+    layer's activations (reading R17).  Written here, independent of
+    the product and of synth/."""
+    a32 = np.ascontiguousarray(a, dtype=np.float32)
+    b = a32.view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32).astype(np.float64).reshape(a32.shape)
+
+
+def mha_layer(x, wq, wk, wv, wo, H: int, D: int, causal: bool = False):
+    """The distributed MHA layer of P:670-675 on one device (NEXT-3):
+    Q, K, V = X W_Q, X W_K, X W_V (fp64 products stored as bf16),
+    Z = attention(Q, K, V) (this oracle; stored as bf16),
+    Y = concat_h(Z) W_0 (P:675), in fp64.  Returns (Y, lse)."""
+    x = np.asarray(x, dtype=np.float64)
+    L = x.shape[0]
+    q = round_bf16(x @ np.asarray(wq, np.float64)).reshape(L, H, D)
+    k = round_bf16(x @ np.asarray(wk, np.float64)).reshape(L, H, D)
+    v = round_bf16(x @ np.asarray(wv, np.float64)).reshape(L, H, D)
+    z, lse = attention(q, k, v, causal)
+    z = round_bf16(z).reshape(L, H * D)
+    return z @ np.asarray(wo, np.float64), lse
+
+
 def attention_flops(L: int, D: int, H: int, causal: bool) -> float:
     """Algorithmic FLOP count of the north_star metric: 4*L^2*D*H, halved if causal."""
     f = 4.0 * L * L * D * H

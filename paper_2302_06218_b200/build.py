@@ -32,6 +32,12 @@ def nccl_root() -> Path:
     return p
 
 
+def cublas_root() -> Path:
+    """cuBLAS of the nvidia wheel torch uses (same soname, loaded once)."""
+    purelib = Path(sysconfig.get_paths()["purelib"])
+    return purelib / "nvidia" / "cublas"
+
+
 def nvcc() -> str:
     for c in ("/usr/local/cuda/bin/nvcc", "nvcc"):
         if os.path.exists(c) or c == "nvcc":
@@ -71,9 +77,10 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> Path:
     if LIB.exists() and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
         return LIB
     nr = nccl_root()
+    cb = cublas_root()
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", *map(str, objs), "-o", str(LIB),
-           "-L", str(nr / "lib"), "-l:libnccl.so.2",
-           "-Xlinker", f"-rpath={nr / 'lib'}"]
+           "-L", str(nr / "lib"), "-l:libnccl.so.2", "-L", str(cb / "lib"), "-l:libcublas.so.12",
+           "-Xlinker", f"-rpath={nr / 'lib'}", "-Xlinker", f"-rpath={cb / 'lib'}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

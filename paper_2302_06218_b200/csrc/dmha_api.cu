@@ -15,6 +15,7 @@
 //   compute:         attention(q_r, kv_s, positions of src) -> partial;
 //                    s = 0 writes the accumulator, s >= 1 combines into it, the
 //                    last step writes out/lse.  P = 1 writes out/lse directly.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -75,6 +76,10 @@ struct State {
   // head-parallel exchange workspace (dmha_forward_headpar*)
   void* hp = nullptr;
   size_t hp_bytes = 0;
+  // NEXT-3 layer workspace (dmha_mha_forward): q, k, v, o, lse; cuBLAS handle
+  void* mha = nullptr;
+  size_t mha_bytes = 0;
+  cublasHandle_t blas = nullptr;
   // host-path staging
   void* st_qkv = nullptr;  // q, k, v back to back
   void* st_out = nullptr;
@@ -155,7 +160,7 @@ void free_ptr(float*& p) {
 
 void update_ws_stat() {
   g.stats.workspace_bytes = 2 * g.kv_bytes + 2 * g.acc_elems * 4 + 2 * g.lse_elems * 4 +
-                            g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes;
+                            g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes + g.mha_bytes;
 }
 
 int alloc_or_oom(void** p, size_t bytes, const char* what) {
@@ -543,6 +548,8 @@ int dmha_finalize(void) {
   free_ptr(g.st_out);
   free_ptr(g.st_lse);
   free_ptr(g.hp);
+  free_ptr(g.mha);
+  if (g.blas) cublasDestroy(g.blas);
   resolve_profiles();
   for (cudaEvent_t e : g.pool) cudaEventDestroy(e);
   g.pool.clear();
@@ -849,6 +856,60 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
   }
   g.stats.forwards++;
   return DMHA_OK;
+}
+
+int dmha_mha_forward(const void* x, const void* wq, const void* wk, const void* wv,
+                     const void* wo, void* y, float* lse, int64_t L, int d_model, int D, int H,
+                     int causal) {
+  if (int rc = check_state()) return rc;
+  if (g.dtype != DMHA_BF16) return fail(DMHA_ERR_UNSUPPORTED, "dmha_mha_forward: bf16 only");
+  if (!x || !wq || !wk || !wv || !wo || !y)
+    return fail(DMHA_ERR_INVALID, "dmha_mha_forward: null pointer");
+  if (d_model < 1 || d_model % 8 != 0)
+    return fail(DMHA_ERR_INVALID, "dmha_mha_forward: d_model must be a positive multiple of 8");
+  if (L < 1 || H < 1 || L % g.world != 0)
+    return fail(DMHA_ERR_INVALID, "dmha_mha_forward: bad L/H for world size %d", g.world);
+  if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_mha_forward: D=%d", D);
+  const int64_t Lloc = L / g.world;
+  const size_t act = static_cast<size_t>(Lloc) * H * D * 2;
+  const size_t lbytes = static_cast<size_t>(Lloc) * H * 4;
+  const size_t need = 4 * act + lbytes + 4 * 256;
+  if (need > g.mha_bytes) {
+    free_ptr(g.mha);
+    g.mha_bytes = 0;
+    if (int rc = alloc_or_oom(&g.mha, need, "MHA layer activations")) return rc;
+    g.mha_bytes = need;
+    update_ws_stat();
+  }
+  if (!g.blas && cublasCreate(&g.blas) != CUBLAS_STATUS_SUCCESS)
+    return fail(DMHA_ERR_CUDA, "dmha_mha_forward: cublasCreate failed");
+  if (cublasSetStream(g.blas, g.stream) != CUBLAS_STATUS_SUCCESS)
+    return fail(DMHA_ERR_CUDA, "dmha_mha_forward: cublasSetStream failed");
+  char* ws = static_cast<char*>(g.mha);
+  char* q = ws;
+  char* k = q + act;
+  char* v = k + act;
+  char* o = v + act;
+  float* l = reinterpret_cast<float*>(o + act);
+  const int HD = H * D;
+  const float one = 1.f, zero = 0.f;
+  // Row-major C[M,N] = A[M,K] B[K,N]  <=>  column-major C^T = B^T A^T.
+  auto gemm = [&](const void* A, const void* B, void* Cm, int64_t M, int N, int K) -> int {
+    cublasStatus_t st = cublasGemmEx(g.blas, CUBLAS_OP_N, CUBLAS_OP_N, N, static_cast<int>(M), K,
+                                     &one, B, CUDA_R_16BF, N, A, CUDA_R_16BF, K, &zero, Cm,
+                                     CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS)
+      return fail(DMHA_ERR_CUDA, "dmha_mha_forward: cublasGemmEx failed (%d)", static_cast<int>(st));
+    return DMHA_OK;
+  };
+  // replicated W_Q, W_K, W_V applied to this rank's rows, all heads.
+  if (int rc = gemm(x, wq, q, Lloc, HD, d_model)) return rc;
+  if (int rc = gemm(x, wk, k, Lloc, HD, d_model)) return rc;
+  if (int rc = gemm(x, wv, v, Lloc, HD, d_model)) return rc;
+  // the distributed attention (ring; same result as the paper's exchange).
+  if (int rc = dmha_forward(q, k, v, o, lse ? lse : l, L, D, H, causal)) return rc;
+  // concatenated heads times the replicated W_0.
+  return gemm(o, wo, y, Lloc, d_model, HD);
 }
 
 int dmha_attention_local(const void* q, const void* k, const void* v, void* out, float* lse,

@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "dmha_forward", "dmha_forward_host", "dmha_forward_emulated", "dmha_workspace_bytes",
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
     "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
-    "dmha_forward_headpar", "dmha_forward_headpar_emulated",
+    "dmha_forward_headpar", "dmha_forward_headpar_emulated", "dmha_mha_forward",
 )
 
 
@@ -86,6 +86,7 @@ def lib():
             "dmha_ring_plan_step": [I, I, I, I, I64, ctypes.POINTER(RingPlan)],
             "dmha_forward_headpar": [P, P, P, P, P, I64, I, I, I],
             "dmha_forward_headpar_emulated": [I, I, P, P, P, P, P, I64, I, I, I],
+            "dmha_mha_forward": [P, P, P, P, P, P, P, I64, I, I, I, I],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -240,6 +241,19 @@ def forward_headpar_emulated(world_size: int, layout, q, k, v, L: int, causal: b
                                                _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
                                                int(bool(causal))))
     return out, lse
+
+
+def mha_forward(x, wq, wk, wv, wo, L: int, H: int, D: int, causal: bool = False, y=None, lse=None):
+    """NEXT-3: distributed MHA layer y = Attn(x W_Q, x W_K, x W_V) W_0 on this
+    rank's rows x [L/P, d_model] (weights replicated)."""
+    import torch
+    Lloc, d_model = x.shape
+    if y is None:
+        y = torch.empty((Lloc, d_model), dtype=x.dtype, device=x.device)
+    set_stream(_cur_stream())
+    _check(lib().dmha_mha_forward(_ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(y), _ptr(lse),
+                                  int(L), int(d_model), int(D), int(H), int(bool(causal))))
+    return y
 
 
 def attention_local(q, k, v, out, lse, causal=False, qmap=None, kmap=None, out_mode: int = 0):

@@ -56,3 +56,14 @@ def one_hot_selector(L: int, H: int, D: int, targets, q_mag: float = 8.0, k_mag:
     k[targets, :, np.arange(D)] = k_mag
     v = normal((L, H, D), seed, 2, dtype)
     return q, k, v
+
+
+def mha_layer(L: int, d_model: int, H: int, D: int, seed: int = 99):
+    """x ~ N(0,1) [L, d_model]; W_Q, W_K, W_V ~ N(0, 1/d_model) [d_model, H*D];
+    W_0 ~ N(0, 1/(H*D)) [H*D, d_model]; all rounded to bf16."""
+    x = normal((L, d_model), seed, 10)
+    wq = normal((d_model, H * D), seed, 11, scale=d_model ** -0.5)
+    wk = normal((d_model, H * D), seed, 12, scale=d_model ** -0.5)
+    wv = normal((d_model, H * D), seed, 13, scale=d_model ** -0.5)
+    wo = normal((H * D, d_model), seed, 14, scale=(H * D) ** -0.5)
+    return x, wq, wk, wv, wo

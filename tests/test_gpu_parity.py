@@ -288,3 +288,21 @@ def test_headpar_requires_divisible_heads(lib_bf16):
     with pytest.raises(dmha.DmhaError) as e:
         dmha.forward_headpar_emulated(2, "contiguous", x, x.clone(), x.clone(), 128, False)
     assert e.value.code == dmha.ERR_INVALID
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("D", [64, 128])
+def test_mha_layer_matches_oracle(lib_bf16, oracle_mod, causal, D):
+    """NEXT-3: the full layer (cuBLAS projections + our attention) vs the
+    oracle layer with the same bf16 storage points (reading R17)."""
+    L, H, d_model = 1000, 4, 256
+    x, wq, wk, wv, wo = inputs.mha_layer(L, d_model, H, D)
+    dev = [to_dev(a) for a in (x, wq, wk, wv, wo)]
+    lse = torch.empty((H, L), dtype=torch.float32, device="cuda")
+    y = dmha.mha_forward(*dev, L, H, D, causal, lse=lse)
+    torch.cuda.synchronize()
+    ref_y, ref_l = oracle_mod.mha_layer(x, wq, wk, wv, wo, H, D, causal)
+    yo = y.float().cpu().numpy()
+    ma, rel = metrics(yo, ref_y)
+    assert rel <= 5e-3 and ma <= 2e-2, (ma, rel)
+    assert np.max(np.abs(lse.cpu().numpy() - ref_l)) <= 2e-2

@@ -199,3 +199,30 @@ def test_input_generator_is_bf16_exact_and_seeded():
     q2, _, _ = inputs.qkv(33, 2, 64, seed=99)
     np.testing.assert_array_equal(q, q2)
     assert abs(float(q.std()) - 1.0) < 0.05
+
+
+def test_mha_layer_oracle_reduces_to_attention_with_identity_weights(oracle_mod):
+    """NEXT-3 oracle pin: with W_Q = W_K = W_V = W_0 = I (d_model = H*D) the
+    layer is the attention of X with itself, up to the bf16 storage of Z."""
+    L, H, D = 64, 2, 8
+    x = inputs.normal((L, H * D), 5, 0)
+    I = np.eye(H * D)
+    y, lse = oracle_mod.mha_layer(x, I, I, I, I, H, D, causal=True)
+    xr = x.astype(np.float64).reshape(L, H, D)
+    z, l2 = oracle_mod.attention(xr, xr, xr, True)
+    np.testing.assert_allclose(y, oracle_mod.round_bf16(z).reshape(L, H * D), rtol=0, atol=0)
+    np.testing.assert_allclose(lse, l2, rtol=0, atol=0)
+    # W_V = 0 -> Y = 0 exactly; W_0 linear: Y(2 W_0) = 2 Y(W_0)
+    y0, _ = oracle_mod.mha_layer(x, I, I, 0 * I, I, H, D)
+    assert np.all(y0 == 0)
+    wo = np.random.default_rng(0).standard_normal((H * D, 5))
+    ya, _ = oracle_mod.mha_layer(x, I, I, I, wo, H, D)
+    yb, _ = oracle_mod.mha_layer(x, I, I, I, 2 * wo, H, D)
+    np.testing.assert_allclose(yb, 2 * ya, rtol=0, atol=1e-12)
+
+
+def test_round_bf16_matches_torch():
+    from oracle import oracle
+    a = np.random.default_rng(1).standard_normal(1000).astype(np.float32) * 100
+    np.testing.assert_array_equal(oracle.round_bf16(a),
+                                  torch.from_numpy(a).to(torch.bfloat16).double().numpy())
