@@ -42,6 +42,9 @@ WORKLOADS = {
                desc="C4 MHA L=262144 D=128 H=16 bf16 strong-scaling sweep"),
     "C5": dict(L=1048576, D=64, H=16, causal=True, dtype="bf16", layout="zigzag",
                desc="C5 million-scale MHA L=1048576 D=64 H=16 bf16 causal"),
+    # A/B-only: C5's head shape at 1/8 of its length (tuning runs, not a bench line)
+    "C5s": dict(L=131072, D=64, H=16, causal=True, dtype="bf16", layout="zigzag",
+                desc="C5-shaped A/B workload L=131072 D=64 H=16 bf16 causal"),
 }
 METRIC = "attention TFLOP/s (4*L^2*D*H, /2 causal)"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}

@@ -34,64 +34,22 @@
 #include <omp.h>
 #endif
 
-/* Returns 0 on success, -1 on bad arguments.
- * rows:   n_rows global query indices (NULL => rows 0..L-1, n_rows must be L)
- * key_begin/key_end: only keys j in [key_begin, key_end) are used
- *                    (the full problem is key_begin=0, key_end=L). */
-int oracle_attention_f64(const double *q, const double *k, const double *v,
-                         int64_t L, int D, int H, int causal,
-                         const int64_t *rows, int64_t n_rows,
-                         int64_t key_begin, int64_t key_end,
-                         double *out, double *lse) {
-  if (!q || !k || !v || !out || !lse || L < 1 || D < 1 || H < 1 || n_rows < 0)
-    return -1;
-  if (key_begin < 0 || key_end > L || key_begin > key_end) return -1;
-  if (!rows && n_rows != L) return -1;
-  const double scale = 1.0 / sqrt((double)D);
-  const int64_t n_items = n_rows * (int64_t)H;
-
-#pragma omp parallel
-  {
-    double *x = (double *)malloc(sizeof(double) * (size_t)(key_end - key_begin + 1));
-#pragma omp for schedule(dynamic, 4)
-    for (int64_t item = 0; item < n_items; ++item) {
-      const int64_t r = item / H;
-      const int h = (int)(item % H);
-      const int64_t t = rows ? rows[r] : r; /* global query position */
-      const double *qt = q + (t * H + h) * (int64_t)D;
-      double *zt = out + (r * H + h) * (int64_t)D;
-      int64_t j_end = key_end;
-      if (causal && j_end > t + 1) j_end = t + 1; /* keep j <= t */
-      /* scores x_j = (Q_t . K_j) / sqrt(D)  (Eq. unnormalized + scale) */
-      double m = -INFINITY;
-      for (int64_t j = key_begin; j < j_end; ++j) {
-        const double *kj = k + (j * H + h) * (int64_t)D;
-        double s = 0.0;
-        for (int d = 0; d < D; ++d) s += qt[d] * kj[d];
-        s *= scale;
-        x[j - key_begin] = s;
-        if (s > m) m = s;
-      }
-      for (int d = 0; d < D; ++d) zt[d] = 0.0;
-      if (j_end <= key_begin) { /* empty key set */
-        lse[(int64_t)h * n_rows + r] = -INFINITY;
-        continue;
-      }
-      /* softmax denominator  sum_j exp(x_j - m) */
-      double l = 0.0;
-      for (int64_t j = key_begin; j < j_end; ++j) l += exp(x[j - key_begin] - m);
-      /* Z_t = sum_j A_{t,j} V_j */
-      for (int64_t j = key_begin; j < j_end; ++j) {
-        const double a = exp(x[j - key_begin] - m) / l;
-        const double *vj = v + (j * H + h) * (int64_t)D;
-        for (int d = 0; d < D; ++d) zt[d] += a * vj[d];
-      }
-      lse[(int64_t)h * n_rows + r] = m + log(l);
-    }
-    free(x);
-  }
-  return 0;
-}
+/* The oracle body is written once (attention_oracle_body.h) and compiled for
+ * two INPUT element types; all arithmetic is fp64 in both:
+ *   oracle_attention_f64   — fp64 inputs
+ *   oracle_attention_f32in — fp32 inputs (the bf16 test inputs are exact in
+ *     fp32), converted element by element to fp64 on load, so large configs
+ *     (C4/C5, GiB-sized K/V) need no fp64 copy.  Same results bit for bit. */
+#define ORACLE_T double
+#define ORACLE_NAME oracle_attention_f64
+#include "attention_oracle_body.h"
+#undef ORACLE_T
+#undef ORACLE_NAME
+#define ORACLE_T float
+#define ORACLE_NAME oracle_attention_f32in
+#include "attention_oracle_body.h"
+#undef ORACLE_T
+#undef ORACLE_NAME
 
 /* Number of OpenMP threads the oracle will use (for the cpu_baseline report). */
 int oracle_num_threads(void) {

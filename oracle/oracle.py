@@ -38,6 +38,7 @@ import numpy as np
 
 _HERE = Path(__file__).resolve().parent
 _SRC = _HERE / "attention_oracle.c"
+_BODY = _HERE / "attention_oracle_body.h"
 _LIB_PATH = _HERE / "build" / "liboracle.so"
 _lib = None
 
@@ -45,7 +46,8 @@ _lib = None
 def build(force: bool = False) -> Path:
     """Compile the C oracle with gcc -O2 -fopenmp (plain C, fp64)."""
     _LIB_PATH.parent.mkdir(parents=True, exist_ok=True)
-    if force or not _LIB_PATH.exists() or _LIB_PATH.stat().st_mtime < _SRC.stat().st_mtime:
+    newest = max(_SRC.stat().st_mtime, _BODY.stat().st_mtime)
+    if force or not _LIB_PATH.exists() or _LIB_PATH.stat().st_mtime < newest:
         # -fno-fast-math: keep IEEE fp64 semantics; no -ffast-math reassociation.
         cmd = ["gcc", "-O2", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
                str(_SRC), "-o", str(_LIB_PATH), "-lm"]
@@ -63,6 +65,8 @@ def _load():
         lib.oracle_attention_f64.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, P, ctypes.c_int64, ctypes.c_int64,
                                              ctypes.c_int64, P, P]
+        lib.oracle_attention_f32in.restype = ctypes.c_int
+        lib.oracle_attention_f32in.argtypes = lib.oracle_attention_f64.argtypes
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -75,9 +79,14 @@ def num_threads() -> int:
 def attention(q, k, v, causal: bool = False, rows=None, key_range=None):
     """C fp64 oracle.  Returns (out [n,H,D] fp64, lse [H,n] fp64)."""
     lib = _load()
-    q = np.ascontiguousarray(q, dtype=np.float64)
-    k = np.ascontiguousarray(k, dtype=np.float64)
-    v = np.ascontiguousarray(v, dtype=np.float64)
+    # fp32 inputs (the bf16-valued test tensors) are read as fp32 and widened
+    # to fp64 on load; anything else is converted to fp64 first.  The
+    # arithmetic is fp64 either way and the results are identical.
+    f32 = all(isinstance(x, np.ndarray) and x.dtype == np.float32 for x in (q, k, v))
+    dt = np.float32 if f32 else np.float64
+    q = np.ascontiguousarray(q, dtype=dt)
+    k = np.ascontiguousarray(k, dtype=dt)
+    v = np.ascontiguousarray(v, dtype=dt)
     L, H, D = q.shape
     assert k.shape == (L, H, D) and v.shape == (L, H, D)
     if rows is None:
@@ -89,7 +98,8 @@ def attention(q, k, v, causal: bool = False, rows=None, key_range=None):
     kb, ke = (0, L) if key_range is None else key_range
     out = np.empty((n, H, D), dtype=np.float64)
     lse = np.empty((H, n), dtype=np.float64)
-    rc = lib.oracle_attention_f64(q.ctypes.data, k.ctypes.data, v.ctypes.data, L, D, H,
+    fn = lib.oracle_attention_f32in if f32 else lib.oracle_attention_f64
+    rc = fn(q.ctypes.data, k.ctypes.data, v.ctypes.data, L, D, H,
                                   int(bool(causal)),
                                   None if rows_arr is None else rows_arr.ctypes.data, n,
                                   int(kb), int(ke), out.ctypes.data, lse.ctypes.data)

@@ -94,8 +94,13 @@ struct Params {
 //  0/2: softmax of Q tile 0/1 saw S(j)   1/3: Q tile 0/1 arrive P(j) ready
 //  4/5: MMA thread saw P0(j)/P1(j) ready   6: MMA thread issued S1(j)
 __device__ __forceinline__ void trace_stamp(const Params& p, int ev, int j) {
-  if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < 4 && j < 64)
+  if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < 2 && j < 64)
     p.trace[(blockIdx.x * 9 + ev) * 64 + j] = clock64();
+}
+// Extra events 0..17 of CTA 0 (stored where CTAs 2-3 would be).
+__device__ __forceinline__ void trace_x(const Params& p, int ev, int j) {
+  if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x == 0 && j < 64)
+    p.trace[(18 + ev) * 64 + j] = clock64();
 }
 
 __device__ __forceinline__ int64_t pos_of(const PosMap& m, int64_t i) {
@@ -127,7 +132,7 @@ __device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
   return static_cast<int>((lim + kBN - 1) / kBN);
 }
 
-template <int D, int kEmu, bool kSplit>
+template <int D, int kEmu, bool kSplit, int kIss>
 __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     ptx::mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&kv_empty[s], kIss == 2 ? 2 : 1);  // one release per issuer
     }
     for (int g = 0; g < 2; ++g) {
       ptx::mbar_init(&s_full[g], 1);
@@ -201,7 +206,9 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       uint32_t phase = 0;
       for (int j = 0; j < nkv; ++j) {
         for (int which = 0; which < 2; ++which) {
+          trace_x(p, 5 + 9 * which, j);
           ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+          trace_x(p, 6 + 9 * which, j);
           ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
           const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
           for (int pn = 0; pn < C::kPanels; ++pn)
@@ -211,8 +218,8 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         }
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == kMmaWarp || (kIss > 1 && warp == kMmaWarp + 1)) {
+    // ------------------------------------------------------------ MMA issuer(s)
     if (lane == 0 && nkv > 0) {
       const uint32_t sq = ptx::smem_u32(sQ);
       const uint32_t skv = ptx::smem_u32(sKV);
@@ -250,44 +257,97 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         // D = 64: P_g has its own TMEM columns, so S_g(j) only waits for the
         // softmax to have LOADED S_g(j-1) (s_free) and runs on the tensor core
         // during that softmax's exponentials; PV_g(j-1) follows when P is ready.
-        // K/V ring item i: K_t = item 2t, V_t = item 2t+1 (load order).
+        // One issuing warp per Q tile (warp kMmaWarp + g): a single thread
+        // issues A-from-TMEM MMAs at only ~69 cycles each whatever N is
+        // (tools/umma_multi.cu: two issuers reach 39, the N = 64 PV needs 32),
+        // and each Q tile's chain no longer waits behind the other's barriers.
+        // K/V ring item i: K_t = item 2t, V_t = item 2t+1 (load order); every
+        // slot is released by both issuers (kv_empty count 2).
+        // kIss = 1: one thread issues both Q tiles (S0 S1, then PV0 PV1);
+        // kIss = 2: warp kMmaWarp + g issues Q tile g (S_g and PV_g);
+        // kIss = 3: warp kMmaWarp issues S0 S1, warp kMmaWarp + 1 PV0 PV1.
+        const int role = warp - kMmaWarp;
+        const int g_lo = kIss == 2 ? role : 0;
+        const int g_hi = kIss == 2 ? g_lo + 1 : 2;
+        const bool do_s = kIss != 3 || role == 0;
+        const bool do_pv = kIss != 3 || role == 1;
+        auto slot_of = [](int item) { return item % C::kStages; };
+        auto par_of = [](int item) { return static_cast<uint32_t>((item / C::kStages) & 1); };
+        ptx::mbar_wait(q_full, 0);
+        if (do_s) {
+          ptx::mbar_wait(&kv_full[slot_of(0)], par_of(0));
+          ptx::tc_fence_after();
+          for (int g = g_lo; g < g_hi; ++g) {
+            qk(g, slot_of(0));
+            ptx::mma_commit(&s_full[g]);
+          }
+          ptx::mma_commit(&kv_empty[slot_of(0)]);
+        }
+        for (int j = 1; j <= nkv; ++j) {
+          const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
+          if (do_s && j < nkv) {  // S_g(j): needs K_j and S_g(j-1) consumed
+            const int ik = 2 * j;
+            trace_x(p, 9 * g_lo + 0, j);
+            ptx::mbar_wait(&kv_full[slot_of(ik)], par_of(ik));
+            trace_x(p, 9 * g_lo + 1, j);
+            for (int g = g_lo; g < g_hi; ++g) {
+              ptx::mbar_wait(&s_free[g], ppar);
+              if (g == g_lo) trace_x(p, 9 * g_lo + 2, j);
+              ptx::tc_fence_after();
+              qk(g, slot_of(ik));
+              ptx::mma_commit(&s_full[g]);
+            }
+            if (g_lo == 0) trace_stamp(p, 6, j);
+            ptx::mma_commit(&kv_empty[slot_of(ik)]);
+          }
+          if (do_pv) {
+            const int iv = 2 * (j - 1) + 1;  // V_{j-1}
+            ptx::mbar_wait(&kv_full[slot_of(iv)], par_of(iv));
+            trace_x(p, 9 * g_lo + 3, j - 1);
+            for (int g = g_lo; g < g_hi; ++g) {
+              ptx::mbar_wait(&p_ready[g], ppar);
+              trace_stamp(p, 4 + g, j - 1);
+              ptx::tc_fence_after();
+              pv_sep(g, slot_of(iv), j > 1);
+              ptx::mma_commit(&pv_done[g]);
+              if (j == nkv) ptx::mma_commit(&o_final[g]);
+            }
+            trace_x(p, 9 * g_lo + 4, j - 1);
+            ptx::mma_commit(&kv_empty[slot_of(iv)]);
+          }
+        }
+      } else if constexpr (kIss == 2) {
+        // D = 128, one issuing warp per Q tile: warp kMmaWarp + g issues
+        // PV_g(j-1) then S_g(j) (same thread, so S_g(j) still follows the PV
+        // that reads P_g(j-1) from S_g's columns, and the S_g(j) commit covers
+        // both).  Every K/V slot is released by both issuers (kv_empty count 2).
+        const int g = warp - kMmaWarp;
         auto slot_of = [](int item) { return item % C::kStages; };
         auto par_of = [](int item) { return static_cast<uint32_t>((item / C::kStages) & 1); };
         ptx::mbar_wait(q_full, 0);
         ptx::mbar_wait(&kv_full[slot_of(0)], par_of(0));
         ptx::tc_fence_after();
-        qk(0, slot_of(0));
-        ptx::mma_commit(&s_full[0]);
-        qk(1, slot_of(0));
-        ptx::mma_commit(&s_full[1]);
+        qk(g, slot_of(0));
+        ptx::mma_commit(&s_full[g]);
         ptx::mma_commit(&kv_empty[slot_of(0)]);
         for (int j = 1; j <= nkv; ++j) {
           const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
-          if (j < nkv) {  // S_g(j): needs K_j and S_g(j-1) consumed
-            const int ik = 2 * j;
-            ptx::mbar_wait(&kv_full[slot_of(ik)], par_of(ik));
-            ptx::mbar_wait(&s_free[0], ppar);
-            ptx::tc_fence_after();
-            qk(0, slot_of(ik));
-            ptx::mma_commit(&s_full[0]);
-            ptx::mbar_wait(&s_free[1], ppar);
-            ptx::tc_fence_after();
-            qk(1, slot_of(ik));
-            ptx::mma_commit(&s_full[1]);
-            trace_stamp(p, 6, j);
-            ptx::mma_commit(&kv_empty[slot_of(ik)]);
-          }
-          const int iv = 2 * (j - 1) + 1;  // V_{j-1}
+          const int iv = 2 * (j - 1) + 1, ik = 2 * j;
           ptx::mbar_wait(&kv_full[slot_of(iv)], par_of(iv));
-          for (int g = 0; g < 2; ++g) {
-            ptx::mbar_wait(&p_ready[g], ppar);
-            trace_stamp(p, 4 + g, j - 1);
-            ptx::tc_fence_after();
-            pv_sep(g, slot_of(iv), j > 1);
-            ptx::mma_commit(&pv_done[g]);
-            if (j == nkv) ptx::mma_commit(&o_final[g]);
-          }
+          if (j < nkv) ptx::mbar_wait(&kv_full[slot_of(ik)], par_of(ik));
+          ptx::mbar_wait(&p_ready[g], ppar);
+          trace_stamp(p, 4 + g, j - 1);
+          ptx::tc_fence_after();
+          pv(g, slot_of(iv), j > 1);
           ptx::mma_commit(&kv_empty[slot_of(iv)]);
+          if (j < nkv) {
+            qk(g, slot_of(ik));
+            ptx::mma_commit(&s_full[g]);
+            if (g == 1) trace_stamp(p, 6, j);
+            ptx::mma_commit(&kv_empty[slot_of(ik)]);
+          } else {
+            ptx::mma_commit(&o_final[g]);
+          }
         }
       } else {
       int stage = 0;
@@ -530,14 +590,6 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         l_run *= alpha;
         m_run = m_new;
       }
-      if constexpr (kSepP) {
-        // P_g(j) and the O_g rescale need PV_g(j-1) finished (usually long done:
-        // it was issued when P_g(j-1) was ready).
-        if (j > 0) {
-          ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
-          ptx::tc_fence_after();
-        }
-      }
       // P = exp2(S*scale*log2e - m) -> bf16, written over the first 64 columns
       // of S (D = 64: into P_g) in 16-column chunks so the fp32 scores die as P
       // is produced.
@@ -546,7 +598,21 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       const uint32_t tP = kSepP ? (tmem + lane_addr + kPCol + g * 128) : tS;
       // Unmasked tiles send kEmu of every 8 column pairs to the FMA-pipe
       // polynomial; masked tiles (-inf entries, exact zeros needed) use MUFU only.
-      if (kEmu == 0 || masked) {
+      if constexpr (kSepP) {
+        // D = 64: exponentials first (in registers), THEN wait for PV_g(j-1) to
+        // have read P_g(j-1) (and to have finished O_g, for the rescale), then
+        // store P_g(j): the PV latency hides behind the MUFU work instead of
+        // sitting between the row max and the exponentials.
+        if (kEmu == 0 || masked)
+          sm::exp_inplace<0>(s, sl2, m_use);
+        else
+          sm::exp_inplace<(kEmu > 4 ? 4 : kEmu)>(s, sl2, m_use);
+        if (j > 0) {
+          ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
+          ptx::tc_fence_after();
+        }
+        l_run += sm::store_p(s, tP);
+      } else if (kEmu == 0 || masked) {
         // scalar FFMA + MUFU.EX2 (the measured-fastest form on B200)
         float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
@@ -680,7 +746,7 @@ bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
   return r == CUDA_SUCCESS;
 }
 
-template <int D, int E, bool S>
+template <int D, int E, bool S, int I = 2>
 cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   using C = Cfg<D>;
   CUtensorMap tq, tk, tv;
@@ -689,7 +755,7 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, S>,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, S, I>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -709,25 +775,40 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H);
-  attn_fwd_sm100_kernel<D, E, S><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  attn_fwd_sm100_kernel<D, E, S, I><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
 
-// DMHA_EMU = pairs (of every 8) of score columns on the FMA-pipe exp2
-// (measurement knob; default 0).
+// Measurement knobs (defaults = the measured-fastest configuration):
+//  DMHA_EMU     = pairs (of every 8) of score columns on the FMA-pipe exp2 (0)
+//  DMHA_ISSUERS = MMA-issuing threads: 1 = one for both Q tiles (D = 128
+//                 default), 2 = one per Q tile, 3 = split S / PV issuers
+//                 (D = 64 only; D = 64 default)
+//  DMHA_SPLIT   = 1: split-row softmax (16 softmax warps)
 template <int D>
 cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   int emu = 0;
   if (const char* e = std::getenv("DMHA_EMU")) emu = std::atoi(e);
+  int iss = D == 64 ? 3 : 1;
+  if (const char* e = std::getenv("DMHA_ISSUERS")) iss = std::atoi(e);
   bool split = false;
   if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
-  if (split) return launch_de<D, 0, true>(a, stream);
+  if (split) return launch_de<D, 0, true, 1>(a, stream);
+  if (iss == 2) return emu == 1 ? launch_de<D, 1, false, 2>(a, stream)
+                                : launch_de<D, 0, false, 2>(a, stream);
+  if (D == 64 && iss == 3) {
+    switch (emu) {
+      case 1: return launch_de<D, 1, false, 3>(a, stream);
+      case 2: return launch_de<D, 2, false, 3>(a, stream);
+      default: return launch_de<D, 0, false, 3>(a, stream);
+    }
+  }
   switch (emu) {
-    case 1: return launch_de<D, 1, false>(a, stream);
-    case 2: return launch_de<D, 2, false>(a, stream);
-    case 8: return launch_de<D, 8, false>(a, stream);  // two-pass exponentials
-    default: return launch_de<D, 0, false>(a, stream);
+    case 1: return launch_de<D, 1, false, 1>(a, stream);
+    case 2: return launch_de<D, 2, false, 1>(a, stream);
+    case 8: return launch_de<D, 8, false, 1>(a, stream);  // two-pass exponentials
+    default: return launch_de<D, 0, false, 1>(a, stream);
   }
 }
 

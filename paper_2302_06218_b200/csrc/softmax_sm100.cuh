@@ -135,6 +135,44 @@ __device__ __forceinline__ float exp_tile_2pass(float (&s)[128], float sl2, floa
   return t.x + t.y;
 }
 
+// In-place exponentials of one 128-column score row (pass 1 of the split
+// exp / store used by the D = 64 schedule, so the wait for the P buffer sits
+// after the MUFU work): s <- exp2(s*scale*log2e - m).  EMU of every 8 column
+// pairs on the FMA-pipe polynomial (finite inputs only), the rest on MUFU.
+template <int EMU>
+__device__ __forceinline__ void exp_inplace(float (&s)[128], float sl2, float m_use) {
+  const float2 sc2 = make_float2(sl2, sl2);
+  const float2 nm2 = make_float2(-m_use, -m_use);
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+    const float2 pe = ((i & 7) < EMU) ? exp2_poly2(x) : exp2_mufu2(x);
+    s[2 * i] = pe.x;
+    s[2 * i + 1] = pe.y;
+  }
+}
+
+// Pass 2: pack the 128 exponentials to bf16, store them as 64 TMEM columns at
+// tP (16-column chunks) and return their fp32 sum.
+__device__ __forceinline__ float store_p(const float (&s)[128], uint32_t tP) {
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                   make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float2 pe = make_float2(s[32 * c + 2 * e], s[32 * c + 2 * e + 1]);
+      acc[e & 3] = __fadd2_rn(acc[e & 3], pe);
+      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
+      pk[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    ptx::tmem_st16(tP + c * 16, pk);
+  }
+  const float2 t = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+  return t.x + t.y;
+}
+
 // Row max of 128 scores as a shallow tree: 16 independent 3-input max chains
 // of depth 4, then a 3-level tree (instead of 4 serial chains of depth 32).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {

@@ -17,11 +17,13 @@ import numpy as np
 
 def round_to_bf16(x: np.ndarray) -> np.ndarray:
     """fp32 -> nearest bf16 (ties to even), returned as fp32 holding bf16 values."""
-    x = np.ascontiguousarray(x, dtype=np.float32)
-    b = x.view(np.uint32).astype(np.uint64)
+    x = np.array(x, dtype=np.float32, copy=True, order="C")
+    b = x.view(np.uint32)  # in place, uint32: no overflow for finite inputs
     lsb = (b >> 16) & 1
-    b = (b + 0x7FFF + lsb) & 0xFFFF0000
-    return b.astype(np.uint32).view(np.float32).reshape(x.shape)
+    b += np.uint32(0x7FFF)
+    b += lsb
+    b &= np.uint32(0xFFFF0000)
+    return x
 
 
 def normal(shape, seed: int, tensor_id: int, dtype: str = "bf16", scale: float = 1.0) -> np.ndarray:

@@ -1,0 +1,103 @@
+"""Sampled parity at BASELINE.json's full sizes (SURVEY §8(c) "Large configs").
+
+The full fp64 oracle is infeasible at C3-C5 (C5 ~ 2e15 FLOP), so each test runs
+the CUDA path on the whole configuration — in the launch configuration
+``bench.py`` times (P = 1 forward) or through the single-GPU emulation of the
+P-rank ring (the same kernels, position maps and combine order as the NCCL
+ring) — and checks a sample of output rows against the oracle computed one row
+at a time over ALL keys:
+  the first and last 64 rows, rows on both sides of every shard / zigzag-chunk
+  boundary (or of sampled CTA boundaries at P = 1), and seeded random rows;
+all heads of each sampled row.  Bar: the north_star bf16 tolerance
+(max abs <= 2e-2, rel L2 <= 5e-3 over the sample; lse abs <= 1e-3).
+Inputs: synth/inputs.py (seeded N(0,1), bf16-rounded), identical bits on both
+sides.
+"""
+import numpy as np
+import pytest
+
+from synth import inputs
+from tests.parity import assert_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2302_06218_b200 import dmha  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    dmha.init(1, 0, None, 0, "bf16", "contiguous")
+    yield
+    dmha.finalize()
+
+
+def _rows(L, boundaries, n_side, n_rand, seed):
+    rows = set(range(64)) | set(range(L - 64, L))
+    for b in boundaries:
+        rows |= set(range(max(0, b - n_side), min(L, b + n_side)))
+    rows |= set(np.random.default_rng(seed).integers(0, L, n_rand).tolist())
+    return np.array(sorted(rows), dtype=np.int64)
+
+
+def _to_dev(x):
+    # fp32 (bf16-valued) -> device, then an exact cast to bf16 on the device
+    return torch.from_numpy(x).cuda().to(torch.bfloat16)
+
+
+def _ring_emulated(P, layout, q, k, v, L, causal):
+    """Shard the global device tensors into [P, L/P, H, D], run the emulated
+    ring, return (out [L, H, D] bf16 on device, lse [H, L] on device) in
+    global row order."""
+    idx = [torch.from_numpy(dmha.global_rows(L, P, r, layout)).cuda() for r in range(P)]
+    dq, dk, dv = (torch.stack([x[i] for i in idx]) for x in (q, k, v))
+    out, lse = dmha.forward_emulated(P, layout, dq, dk, dv, L, causal)
+    torch.cuda.synchronize()
+    del dq, dk, dv
+    pos = torch.cat(idx)
+    out_g = torch.empty_like(q)
+    out_g[pos] = out.reshape(-1, *q.shape[1:])
+    lse_g = torch.empty((q.shape[1], L), dtype=torch.float32, device=q.device)
+    lse_g[:, pos] = lse.permute(1, 0, 2).reshape(q.shape[1], -1)
+    return out_g, lse_g
+
+
+def _check(out_dev, lse_dev, q, k, v, causal, rows, oracle_mod, what):
+    r = torch.from_numpy(rows).cuda()
+    got_o = out_dev[r].float().cpu().numpy()
+    got_l = lse_dev[:, r].cpu().numpy()
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal, rows=rows)
+    ma, rel = assert_parity(got_o, got_l, ref_o, ref_l, "bf16", what)
+    print(f"{what}: {rows.size} rows x {q.shape[1]} heads  max abs {ma:.3e}  rel L2 {rel:.3e}")
+
+
+def test_c4_p1_bench_configuration(oracle_mod):
+    """C4 at N = 1 exactly as bench.py times it: L=262144, D=128, H=16,
+    non-causal, one dmha_forward over the whole sequence."""
+    L, H, D = 262144, 16, 128
+    q, k, v = inputs.qkv(L, H, D, seed=1237)
+    dq, dk, dv = _to_dev(q), _to_dev(k), _to_dev(v)
+    out, lse = dmha.forward(dq, dk, dv, L, False)
+    torch.cuda.synchronize()
+    rows = _rows(L, [256 * i for i in range(1, L // 256, 97)], 8, 96, seed=4)
+    _check(out, lse, q, k, v, False, rows, oracle_mod, "C4 P=1")
+
+
+def test_c3_ring_p4_contiguous(oracle_mod):
+    """C3: L=131072, D=128, H=8, non-causal, P=4 contiguous shards (emulated ring)."""
+    L, H, D, P = 131072, 8, 128, 4
+    q, k, v = inputs.qkv(L, H, D, seed=1236)
+    out, lse = _ring_emulated(P, "contiguous", _to_dev(q), _to_dev(k), _to_dev(v), L, False)
+    rows = _rows(L, [r * (L // P) for r in range(1, P)], 32, 128, seed=3)
+    _check(out, lse, q, k, v, False, rows, oracle_mod, "C3 ring P=4")
+
+
+def test_c5_ring_p8_zigzag_causal(oracle_mod):
+    """C5: L=2^20, D=64, H=16, causal, P=8 zigzag shards (emulated ring) — the
+    million-scale configuration of BASELINE.json."""
+    L, H, D, P = 1 << 20, 16, 64, 8
+    q, k, v = inputs.qkv(L, H, D, seed=1238)
+    out, lse = _ring_emulated(P, "zigzag", _to_dev(q), _to_dev(k), _to_dev(v), L, True)
+    chunk = L // (2 * P)
+    rows = _rows(L, [c * chunk for c in range(1, 2 * P)], 16, 96, seed=5)
+    _check(out, lse, q, k, v, True, rows, oracle_mod, "C5 ring P=8 zigzag")

@@ -226,3 +226,16 @@ def test_round_bf16_matches_torch():
     a = np.random.default_rng(1).standard_normal(1000).astype(np.float32) * 100
     np.testing.assert_array_equal(oracle.round_bf16(a),
                                   torch.from_numpy(a).to(torch.bfloat16).double().numpy())
+
+
+def test_fp32_input_entry_identical_to_fp64(oracle_mod):
+    """oracle_attention_f32in (fp32 inputs widened on load, used for the
+    GiB-sized sampled-parity configs) gives the same bits as the fp64 entry."""
+    q, k, v = inputs.qkv(333, 3, 64, seed=21)
+    rows = np.array([0, 5, 100, 332], dtype=np.int64)
+    for causal in (False, True):
+        a = oracle_mod.attention(q, k, v, causal, rows=rows, key_range=(7, 300))
+        b = oracle_mod.attention(*(x.astype(np.float64) for x in (q, k, v)), causal, rows=rows,
+                                 key_range=(7, 300))
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])

@@ -19,7 +19,7 @@ dmha.forward(q, k, v, L, False)
 torch.cuda.synchronize()
 dmha.debug_set_trace(None)
 t = buf.view(4, 9, 64).cpu().numpy().astype(np.int64)
-for c in range(2):
+for c in range(int(os.environ.get("TCTAS", 2))):
     tc = t[c] - t[c][0][0]
     print(f"CTA {c}: rows = tile j; cols = 0:WG0 saw S 1:WG0 P 2:WG1 saw S 3:WG1 P 4:mma saw P 5:mma PV issued 6:mma S issued 7:mma saw V landed 8:producer issued V load")
     for j in range(8, 16):
@@ -36,3 +36,15 @@ for c in range(2):
         print(f"  WG0 per tile: S load {ld:.0f}  max+decision {mx:.0f}  exp+store+arrive {ex:.0f}")
     print(f"  period/tile {per:.0f}  softmax WG0 {sm0:.0f}  WG1 {sm1:.0f}  wait-S WG0 {w0:.0f}  WG1 {w1:.0f}  P->mma-sees {lat0:.0f}")
 dmha.finalize()
+# Extra events of CTA 0 (D = 64 kernel): per issuer g (base 9g):
+#  0 before K_j wait, 1 K_j landed, 2 s_free seen, 3 V_{j-1} landed, 4 PV_{j-1} committed;
+#  producer: 5/14 before kv_empty wait for K_j / V_j, 6/15 slot free
+x = buf.view(-1)[18 * 64: 36 * 64].view(18, 64).cpu().numpy().astype(np.int64)
+if x[0][10]:
+    x0 = t[0][0][0]
+    names = ["g0 preK", "g0 Kland", "g0 sfree", "g0 Vland", "g0 PVdone", "prodK pre", "prodK free", "", "",
+             "g1 preK", "g1 Kland", "g1 sfree", "g1 Vland", "g1 PVdone", "prodV pre", "prodV free", "", ""]
+    print("extra events (CTA 0, relative to WG0 first S):")
+    print("  j " + " ".join(f"{n:>10s}" for n in names if n))
+    for j in range(8, 16):
+        print(f"{j:3d} " + " ".join(f"{x[e][j] - x0:10d}" if x[e][j] else "         -" for e in range(18) if names[e]))
