@@ -174,7 +174,9 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     ptx::mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], kIss == 2 ? 2 : 1);  // one release per issuer
+      // one release per issuer that reads the slot (kIss = 4: V slots — the odd
+      // ones, kStages is even — are read by both PV issuers)
+      ptx::mbar_init(&kv_empty[s], (kIss == 2 || (kIss == 4 && (s & 1))) ? 2 : 1);
     }
     for (int g = 0; g < 2; ++g) {
       ptx::mbar_init(&s_full[g], 1);
@@ -218,7 +220,8 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         }
       }
     }
-  } else if (warp == kMmaWarp || (kIss > 1 && warp == kMmaWarp + 1)) {
+  } else if (warp == kMmaWarp || (kIss > 1 && warp == kMmaWarp + 1) ||
+             (kIss == 4 && warp == kMmaWarp + 2)) {
     // ------------------------------------------------------------ MMA issuer(s)
     if (lane == 0 && nkv > 0) {
       const uint32_t sq = ptx::smem_u32(sQ);
@@ -266,11 +269,13 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         // kIss = 1: one thread issues both Q tiles (S0 S1, then PV0 PV1);
         // kIss = 2: warp kMmaWarp + g issues Q tile g (S_g and PV_g);
         // kIss = 3: warp kMmaWarp issues S0 S1, warp kMmaWarp + 1 PV0 PV1.
+        // kIss = 4: warp kMmaWarp issues S0 S1, warp kMmaWarp + 1 + g PV_g.
+        static_assert(C::kStages % 2 == 0, "K and V must keep their slot parity");
         const int role = warp - kMmaWarp;
-        const int g_lo = kIss == 2 ? role : 0;
-        const int g_hi = kIss == 2 ? g_lo + 1 : 2;
-        const bool do_s = kIss != 3 || role == 0;
-        const bool do_pv = kIss != 3 || role == 1;
+        const int g_lo = kIss == 2 ? role : (kIss == 4 && role > 0 ? role - 1 : 0);
+        const int g_hi = (kIss == 2 || (kIss == 4 && role > 0)) ? g_lo + 1 : 2;
+        const bool do_s = (kIss != 3 && kIss != 4) || role == 0;
+        const bool do_pv = (kIss != 3 && kIss != 4) || role >= 1;
         auto slot_of = [](int item) { return item % C::kStages; };
         auto par_of = [](int item) { return static_cast<uint32_t>((item / C::kStages) & 1); };
         ptx::mbar_wait(q_full, 0);
@@ -784,7 +789,8 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
 //  DMHA_EMU     = pairs (of every 8) of score columns on the FMA-pipe exp2 (0)
 //  DMHA_ISSUERS = MMA-issuing threads: 1 = one for both Q tiles (D = 128
 //                 default), 2 = one per Q tile, 3 = split S / PV issuers
-//                 (D = 64 only; D = 64 default)
+//                 (D = 64 only; D = 64 default), 4 = S issuer + one PV issuer
+//                 per Q tile (D = 64 only)
 //  DMHA_SPLIT   = 1: split-row softmax (16 softmax warps)
 template <int D>
 cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
@@ -797,6 +803,7 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   if (split) return launch_de<D, 0, true, 1>(a, stream);
   if (iss == 2) return emu == 1 ? launch_de<D, 1, false, 2>(a, stream)
                                 : launch_de<D, 0, false, 2>(a, stream);
+  if (D == 64 && iss == 4) return launch_de<D, 0, false, 4>(a, stream);
   if (D == 64 && iss == 3) {
     switch (emu) {
       case 1: return launch_de<D, 1, false, 3>(a, stream);
