@@ -746,8 +746,16 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
 
 unsigned long long* g_trace = nullptr;
 
+bool pingpong_fused_combine_ok();  // attn_fwd_sm100_v1.cu
+
+bool attn_fused_combine_supported(int D) {
+  return (D == 64 || D == 128) && kernel_kind(D) == K_PINGPONG && pingpong_fused_combine_ok();
+}
+
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream) {
   if (a.Lq <= 0) return cudaSuccess;
+  if (a.out_mode >= OUT_COMBINE_ACC && !attn_fused_combine_supported(a.D))
+    return cudaErrorInvalidValue;
   if (a.Lq > INT32_MAX || a.Lk > INT32_MAX) return cudaErrorInvalidValue;
   if (kernel_kind(a.D) == K_PINGPONG) return launch_attn_fwd_bf16_pingpong(a, stream);
   if (a.D == 64) return launch_d<64>(a, stream);

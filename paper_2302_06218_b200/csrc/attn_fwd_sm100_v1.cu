@@ -40,6 +40,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "combine_math.cuh"
 #include "kernels.h"
 #include "ptx_sm100.cuh"
 #include "softmax_sm100.cuh"
@@ -85,6 +86,8 @@ struct Params {
   void* out;
   float* lse;
   int out_mode;
+  float* acc_o;    // OUT_COMBINE_*: running accumulator (read; ACC also writes it)
+  float* acc_lse;
   int n_mblk;
   unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
@@ -520,8 +523,8 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            dst[e] = make_float4(o[4 * e] * inv_l, o[4 * e + 1] * inv_l, o[4 * e + 2] * inv_l,
-                                 o[4 * e + 3] * inv_l);
+            dst[e] = make_float4(__fmul_rn(o[4 * e], inv_l), __fmul_rn(o[4 * e + 1], inv_l),
+                                 __fmul_rn(o[4 * e + 2], inv_l), __fmul_rn(o[4 * e + 3], inv_l));
         } else {
           uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
                                                 c * 32);
@@ -666,9 +669,17 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     // ---------------------------------------------------------- epilogue
     const bool empty = !(l_run > 0.f);
     const float inv_l = empty ? 0.f : 1.f / l_run;
-    if (row_ok)
-      p.lse[static_cast<int64_t>(head) * p.Lq + row] =
-          empty ? -INFINITY : (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+    const float lse_s = empty ? -INFINITY : (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+    const int64_t li = static_cast<int64_t>(head) * p.Lq + row;
+    // NEXT-2 fused combine: merge with the running accumulator here instead of
+    // writing an fp32 partial for lse_combine (same arithmetic, same bits).
+    const bool fused = p.out_mode >= OUT_COMBINE_ACC;
+    float wa = 0.f, wp = 0.f, lnew = lse_s;
+    if (fused && row_ok) merge_weights(p.acc_lse[li], lse_s, wa, wp, lnew);
+    if (row_ok) {
+      if (p.out_mode == OUT_COMBINE_ACC) p.acc_lse[li] = lnew;
+      else p.lse[li] = lnew;
+    }
     const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D);
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
@@ -680,13 +691,42 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = 0.f;
       }
-      if (row_ok) {
+      if (row_ok && fused) {
+        float4* acc = reinterpret_cast<float4*>(p.acc_o + obase + c * 32);
+        float r[32];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float4 a4 = acc[e];
+          r[4 * e + 0] = combine_one(a4.x, __fmul_rn(o[4 * e + 0], inv_l), wa, wp);
+          r[4 * e + 1] = combine_one(a4.y, __fmul_rn(o[4 * e + 1], inv_l), wa, wp);
+          r[4 * e + 2] = combine_one(a4.z, __fmul_rn(o[4 * e + 2], inv_l), wa, wp);
+          r[4 * e + 3] = combine_one(a4.w, __fmul_rn(o[4 * e + 3], inv_l), wa, wp);
+        }
+        if (p.out_mode == OUT_COMBINE_ACC) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            acc[e] = make_float4(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
+                                                c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t w[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(r[8 * e + 2 * t], r[8 * e + 2 * t + 1]);
+              w[t] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      } else if (row_ok) {
         if (p.out_mode == OUT_PARTIAL_F32) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            dst[e] = make_float4(o[4 * e] * inv_l, o[4 * e + 1] * inv_l, o[4 * e + 2] * inv_l,
-                                 o[4 * e + 3] * inv_l);
+            dst[e] = make_float4(__fmul_rn(o[4 * e], inv_l), __fmul_rn(o[4 * e + 1], inv_l),
+                                 __fmul_rn(o[4 * e + 2], inv_l), __fmul_rn(o[4 * e + 3], inv_l));
         } else {
           uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
                                                 c * 32);
@@ -777,6 +817,8 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.out = a.out;
   p.lse = a.lse;
   p.out_mode = a.out_mode;
+  p.acc_o = a.acc_o;
+  p.acc_lse = a.acc_lse;
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H);
@@ -800,7 +842,10 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   if (const char* e = std::getenv("DMHA_ISSUERS")) iss = std::atoi(e);
   bool split = false;
   if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
-  if (split) return launch_de<D, 0, true, 1>(a, stream);
+  if (split) {
+    if (a.out_mode >= OUT_COMBINE_ACC) return cudaErrorInvalidValue;  // see pingpong_fused_combine_ok
+    return launch_de<D, 0, true, 1>(a, stream);
+  }
   if (iss == 2) return emu == 1 ? launch_de<D, 1, false, 2>(a, stream)
                                 : launch_de<D, 0, false, 2>(a, stream);
   if (D == 64 && iss == 4) return launch_de<D, 0, false, 4>(a, stream);
@@ -820,6 +865,13 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace
+
+// The fused combine lives in the one-thread-per-row epilogue; the split
+// softmax (two threads per row, DMHA_SPLIT=1) keeps the separate combine.
+bool pingpong_fused_combine_ok() {
+  const char* e = std::getenv("DMHA_SPLIT");
+  return !(e && std::atoi(e) != 0);
+}
 
 cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t stream) {
   if (a.Lq <= 0) return cudaSuccess;

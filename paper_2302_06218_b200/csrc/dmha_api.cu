@@ -72,7 +72,7 @@ struct State {
   float* o_part = nullptr;
   float* lse_acc = nullptr;
   float* lse_part = nullptr;
-  size_t kv_bytes = 0, acc_elems = 0, lse_elems = 0;
+  size_t kv_bytes = 0, acc_elems = 0, lse_elems = 0, part_elems = 0, part_lse_elems = 0;
   // head-parallel exchange workspace (dmha_forward_headpar*)
   void* hp = nullptr;
   size_t hp_bytes = 0;
@@ -159,7 +159,8 @@ void free_ptr(float*& p) {
 }
 
 void update_ws_stat() {
-  g.stats.workspace_bytes = 2 * g.kv_bytes + 2 * g.acc_elems * 4 + 2 * g.lse_elems * 4 +
+  g.stats.workspace_bytes = 2 * g.kv_bytes + (g.acc_elems + g.part_elems) * 4 +
+                            (g.lse_elems + g.part_lse_elems) * 4 +
                             g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes + g.mha_bytes;
 }
 
@@ -174,37 +175,56 @@ int alloc_or_oom(void** p, size_t bytes, const char* what) {
   return DMHA_OK;
 }
 
-// Ring accumulators (always) and K/V ring buffers (need_kv).
+// NEXT-2: the attention epilogue merges each ring-step partial into the
+// accumulator itself (bf16 ping-pong kernel; DMHA_FUSED_COMBINE=0 forces the
+// separate lse_combine pass for A/B), so O_part / lse_part are not needed.
+bool fused_combine(int D) {
+  const char* e = std::getenv("DMHA_FUSED_COMBINE");
+  if (e && std::atoi(e) == 0) return false;
+  return g.dtype == DMHA_BF16 && dmha::attn_fused_combine_supported(D);
+}
+
+// Ring accumulators (always), the partial buffers (unfused combine only) and
+// the K/V ring buffers (need_kv).
 int ensure_ring_ws(int64_t Lloc, int D, int H, bool need_kv) {
   const size_t elems = static_cast<size_t>(Lloc) * H * D;
   const size_t lse = static_cast<size_t>(Lloc) * H;
+  const bool need_part = !fused_combine(D);
   if (elems > g.acc_elems) {
     free_ptr(g.o_acc);
-    free_ptr(g.o_part);
     g.acc_elems = 0;
-    int rc = alloc_or_oom(reinterpret_cast<void**>(&g.o_acc), elems * 4, "O_acc");
-    if (!rc) rc = alloc_or_oom(reinterpret_cast<void**>(&g.o_part), elems * 4, "O_part");
-    if (rc) {
-      free_ptr(g.o_acc);
-      free_ptr(g.o_part);
+    if (int rc = alloc_or_oom(reinterpret_cast<void**>(&g.o_acc), elems * 4, "O_acc")) {
       update_ws_stat();
       return rc;
     }
     g.acc_elems = elems;
   }
+  if (need_part && elems > g.part_elems) {
+    free_ptr(g.o_part);
+    g.part_elems = 0;
+    if (int rc = alloc_or_oom(reinterpret_cast<void**>(&g.o_part), elems * 4, "O_part")) {
+      update_ws_stat();
+      return rc;
+    }
+    g.part_elems = elems;
+  }
   if (lse > g.lse_elems) {
     free_ptr(g.lse_acc);
-    free_ptr(g.lse_part);
     g.lse_elems = 0;
-    int rc = alloc_or_oom(reinterpret_cast<void**>(&g.lse_acc), lse * 4, "lse_acc");
-    if (!rc) rc = alloc_or_oom(reinterpret_cast<void**>(&g.lse_part), lse * 4, "lse_part");
-    if (rc) {
-      free_ptr(g.lse_acc);
-      free_ptr(g.lse_part);
+    if (int rc = alloc_or_oom(reinterpret_cast<void**>(&g.lse_acc), lse * 4, "lse_acc")) {
       update_ws_stat();
       return rc;
     }
     g.lse_elems = lse;
+  }
+  if (need_part && lse > g.part_lse_elems) {
+    free_ptr(g.lse_part);
+    g.part_lse_elems = 0;
+    if (int rc = alloc_or_oom(reinterpret_cast<void**>(&g.lse_part), lse * 4, "lse_part")) {
+      update_ws_stat();
+      return rc;
+    }
+    g.part_lse_elems = lse;
   }
   if (need_kv) {
     const size_t kvb = 2 * elems * elem_bytes(g.dtype);
@@ -279,8 +299,10 @@ int validate(const void* q, const void* k, const void* v, const void* out, const
 
 int run_local(const void* q, const void* k, const void* v, void* out, float* lse, int64_t Lq,
               int64_t Lk, int D, int H, int causal, dmha::PosMap qm, dmha::PosMap km,
-              int out_mode) {
+              int out_mode, float* acc_o = nullptr, float* acc_lse = nullptr) {
   dmha::LocalAttnArgs a;
+  a.acc_o = acc_o;
+  a.acc_lse = acc_lse;
   a.q = q;
   a.k = k;
   a.v = v;
@@ -357,6 +379,12 @@ int ring_compute_step(int s, int P, int r, int layout, const void* q, const void
       return run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
                        dmha::OUT_PARTIAL_F32);
     default: {
+      const bool fin = pl.output == DMHA_PLAN_COMBINE_FINAL;
+      if (fused_combine(D))  // NEXT-2: merge inside the attention epilogue
+        return run_local(q, ks, vs, fin ? out : static_cast<void*>(g.o_acc), fin ? lse : g.lse_acc,
+                         Lloc, Lloc, D, H, causal, qm, km,
+                         fin ? dmha::OUT_COMBINE_FINAL : dmha::OUT_COMBINE_ACC, g.o_acc,
+                         g.lse_acc);
       int rc = run_local(q, ks, vs, g.o_part, g.lse_part, Lloc, Lloc, D, H, causal, qm, km,
                          dmha::OUT_PARTIAL_F32);
       if (rc) return rc;
@@ -572,7 +600,8 @@ int dmha_workspace_bytes(int64_t L, int D, int H, size_t* bytes_out) {
   }
   const size_t elems = static_cast<size_t>(L / g.world) * H * D;
   const size_t lse = static_cast<size_t>(L / g.world) * H;
-  *bytes_out = 2 * (2 * elems * elem_bytes(g.dtype)) + 2 * elems * 4 + 2 * lse * 4;
+  const size_t parts = fused_combine(D) ? 1 : 2;  // O_acc (+ O_part unless fused)
+  *bytes_out = 2 * (2 * elems * elem_bytes(g.dtype)) + parts * (elems * 4 + lse * 4);
   return DMHA_OK;
 }
 

@@ -14,7 +14,11 @@ struct PosMap {
   int64_t chunk;
 };
 
-enum OutMode { OUT_FINAL = 0, OUT_PARTIAL_F32 = 1 };
+// OUT_COMBINE_*: NEXT-2 fused combine — the epilogue merges its partial into
+// (acc_o, acc_lse) itself (combine_math.cuh) and writes either the updated
+// accumulator (ACC, in place) or the final output (FINAL: out/lse in the init
+// dtype), so no fp32 partial goes through HBM.
+enum OutMode { OUT_FINAL = 0, OUT_PARTIAL_F32 = 1, OUT_COMBINE_ACC = 2, OUT_COMBINE_FINAL = 3 };
 
 struct LocalAttnArgs {
   const void* q;
@@ -27,6 +31,8 @@ struct LocalAttnArgs {
   int causal;
   PosMap qmap, kmap;
   int out_mode;
+  float* acc_o = nullptr;    // OUT_COMBINE_*: running O_acc [Lq, H, D] fp32
+  float* acc_lse = nullptr;  // OUT_COMBINE_*: running lse_acc [H, Lq]
 };
 
 // bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu): picks
@@ -34,6 +40,9 @@ struct LocalAttnArgs {
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream);
 // Two query tiles per CTA, ping-pong on the tensor core (attn_fwd_sm100_v1.cu).
 cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t stream);
+// Whether launch_attn_fwd_bf16 accepts OUT_COMBINE_* for head dim D (the
+// ping-pong kernel with the one-thread-per-row epilogue does).
+bool attn_fused_combine_supported(int D);
 // fp32 path (attn_fwd_fp32.cu).
 cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
 // log-sum-exp combine (lse_combine.cu).  out_dtype_bf16 selects the final

@@ -19,28 +19,11 @@
 #include <cmath>
 #include <cstdint>
 
+#include "combine_math.cuh"
 #include "kernels.h"
 
 namespace dmha {
 namespace {
-
-__device__ __forceinline__ void merge_weights(float la, float lp, float& wa, float& wp,
-                                              float& lnew) {
-  const float M = fmaxf(la, lp);
-  if (M == -INFINITY) {  // both empty
-    wa = 0.f;
-    wp = 0.f;
-    lnew = -INFINITY;
-    return;
-  }
-  const float ea = __expf(la - M);  // exp(-inf) = 0
-  const float ep = __expf(lp - M);
-  const float s = ea + ep;
-  lnew = M + __logf(s);
-  const float inv = 1.f / s;
-  wa = ea * inv;
-  wp = ep * inv;
-}
 
 template <int D, bool kFinal, bool kBf16>
 __global__ void __launch_bounds__(256) lse_combine_kernel(float* __restrict__ o_acc,
@@ -63,10 +46,10 @@ __global__ void __launch_bounds__(256) lse_combine_kernel(float* __restrict__ o_
     const float4 a = reinterpret_cast<const float4*>(o_acc)[i];
     const float4 b = reinterpret_cast<const float4*>(o_part)[i];
     float4 r;
-    r.x = (wa == 0.f ? 0.f : a.x * wa) + (wp == 0.f ? 0.f : b.x * wp);
-    r.y = (wa == 0.f ? 0.f : a.y * wa) + (wp == 0.f ? 0.f : b.y * wp);
-    r.z = (wa == 0.f ? 0.f : a.z * wa) + (wp == 0.f ? 0.f : b.z * wp);
-    r.w = (wa == 0.f ? 0.f : a.w * wa) + (wp == 0.f ? 0.f : b.w * wp);
+    r.x = combine_one(a.x, b.x, wa, wp);
+    r.y = combine_one(a.y, b.y, wa, wp);
+    r.z = combine_one(a.z, b.z, wa, wp);
+    r.w = combine_one(a.w, b.w, wa, wp);
     const bool lead = (i - rh * kVecPerRow) == 0;
     if (kFinal) {
       if (kBf16) {

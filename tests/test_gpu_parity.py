@@ -306,3 +306,30 @@ def test_mha_layer_matches_oracle(lib_bf16, oracle_mod, causal, D):
     ma, rel = metrics(yo, ref_y)
     assert rel <= 5e-3 and ma <= 2e-2, (ma, rel)
     assert np.max(np.abs(lse.cpu().numpy() - ref_l)) <= 2e-2
+
+
+@pytest.mark.parametrize("P,layout,causal,D", [(2, "contiguous", False, 128), (4, "zigzag", True, 64),
+                                               (8, "zigzag", True, 128), (3, "contiguous", True, 64)])
+def test_fused_combine_bit_identical_to_separate_pass(lib_bf16, oracle_mod, monkeypatch, P, layout,
+                                                      causal, D):
+    """NEXT-2: the epilogue-fused LSE combine (default) gives exactly the bits
+    of the separate lse_combine pass (shared combine_math.cuh, _rn arithmetic),
+    and both match the oracle."""
+    H = 2
+    L = P * 777 if layout == "contiguous" else 2 * P * 389  # ragged shards
+    q, k, v = inputs.qkv(L, H, D, seed=900 + P)
+    parts = [[dmha.shard(x, P, r, layout) for r in range(P)] for x in (q, k, v)]
+    dq, dk, dv = (to_dev(np.stack(p)) for p in parts)
+    res = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("DMHA_FUSED_COMBINE", fused)
+        o, l = dmha.forward_emulated(P, layout, dq, dk, dv, L, causal)
+        torch.cuda.synchronize()
+        res[fused] = (o.float().cpu().numpy(), l.cpu().numpy())
+    np.testing.assert_array_equal(res["1"][0], res["0"][0])
+    np.testing.assert_array_equal(res["1"][1], res["0"][1])
+    out_g = dmha.unshard(list(res["1"][0]), L, layout)
+    lse_g = dmha.unshard([x.T for x in res["1"][1]], L, layout).T
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(out_g, lse_g, ref_o, ref_l, "bf16", f"fused ring P={P} {layout} causal={causal}")
+

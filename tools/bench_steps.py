@@ -96,21 +96,28 @@ def main():
         print(json.dumps(rec), flush=True)
         del oa, op, la, lp, out, lo
 
-    # whole per-rank ring compute through the emulation (C3 size, P = 2, 4, 8)
-    L, D, H = 131072, 128, 8
-    for P in (2, 4, 8):
+    # whole per-rank ring compute through the emulation (C3 size P = 2, 4, 8;
+    # C4 P = 8), with the NEXT-2 fused combine (default) and the separate pass
+    cases = [(131072, 128, 8, P) for P in (2, 4, 8)] + [(262144, 128, 16, 8)]
+    for L, D, H, P in cases:
         for layout, causal in (("contiguous", False), ("zigzag", True)):
+            if L == 262144 and causal:
+                continue
             Ll = L // P
             q, k, v = (torch.randn(P, Ll, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
             out = torch.empty_like(q)
             lse = torch.empty(P, H, Ll, device="cuda")
-            ms = time_cuda(lambda: dmha.forward_emulated(P, layout, q, k, v, L, causal, out, lse), iters=3, warmup=1)
-            tf = attn_flops(L, D, H, causal) / ms / 1e9  # all P ranks' work, serialised on one GPU
-            rec = {"P": P, "layout": layout, "causal": causal, "L": L, "D": D, "H": H,
-                   "ms_all_ranks_serial": ms, "tflops_serial": tf,
-                   "projected_ms_per_rank_if_perfectly_parallel": ms / P}
-            res["ring_emulated"].append(rec)
-            print(json.dumps(rec), flush=True)
+            for fused in ("1", "0"):
+                os.environ["DMHA_FUSED_COMBINE"] = fused
+                ms = time_cuda(lambda: dmha.forward_emulated(P, layout, q, k, v, L, causal, out, lse),
+                               iters=3 if L < 262144 else 2, warmup=1)
+                tf = attn_flops(L, D, H, causal) / ms / 1e9  # all P ranks' work, serialised on one GPU
+                rec = {"P": P, "layout": layout, "causal": causal, "L": L, "D": D, "H": H,
+                       "fused_combine": fused == "1", "ms_all_ranks_serial": ms, "tflops_serial": tf,
+                       "projected_ms_per_rank_if_perfectly_parallel": ms / P}
+                res["ring_emulated"].append(rec)
+                print(json.dumps(rec), flush=True)
+            os.environ.pop("DMHA_FUSED_COMBINE", None)
             del q, k, v, out, lse
             torch.cuda.empty_cache()
     dmha.finalize()
