@@ -106,8 +106,11 @@ const char *dmha_last_error(void);
  * [H, L_loc] fp32.  L is the GLOBAL length (L % P == 0; % 2P for ZIGZAG), D the
  * per-head dim (64 or 128), H >= 1 heads, causal 0/1.  All ranks must call with
  * identical (L, D, H, causal).  Ring: P-1 steps of ncclSend/ncclRecv of (K,V)
- * to rank+1 / from rank-1 overlapped with the local attention kernel, then an
- * fp32 log-sum-exp combine of the per-step partials.
+ * to rank+1 / from rank-1 overlapped with the local attention kernel, and an
+ * fp32 log-sum-exp combine of the per-step partials into a running
+ * accumulator (north_star (3)) — for bf16 fused into the attention kernel's
+ * epilogue (env DMHA_FUSED_COMBINE=0 selects the
+ * separate combine kernel, bit-identical result).
  * Errors: INVALID (null, sizes, misaligned, out/lse overlapping q/k/v),
  * UNSUPPORTED (D), STATE, OOM, CUDA, NCCL. */
 int dmha_forward(const void *q, const void *k, const void *v, void *out, float *lse,
@@ -161,8 +164,11 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void *q, con
                                   const void *v, void *out, float *lse, int64_t L, int D, int H,
                                   int causal);
 
-/* Device bytes the library will hold per rank for (L, D, H) at the initialised
- * world size and dtype (ring buffers + fp32 accumulators + staging excluded). */
+/* Device bytes the ring will hold per rank for (L, D, H) at the initialised
+ * world size and dtype: 2 K/V receive buffers (2 * 2 * L_loc*H*D*elem) + the
+ * fp32 accumulator O_acc and lse_acc (+ the O_part / lse_part partial buffers
+ * when the combine is not fused).  0 at world size 1.  Staging buffers of
+ * dmha_forward_host are not included. */
 int dmha_workspace_bytes(int64_t L, int D, int H, size_t *bytes_out);
 
 /* Synchronises outstanding profiled work, then copies the counters. */
