@@ -236,6 +236,39 @@ int dmha_attention_local(const void *q, const void *k, const void *v, void *out,
 int dmha_lse_combine(float *o_acc, float *lse_acc, const float *o_part, const float *lse_part,
                      void *out, float *lse_out, int64_t Lq, int D, int H, int final_step);
 
+/* ---- NEXT-4: the token Selector (§10.2) ------------------------ */
+
+/* Scorers for s_{psi,tau} — the paper never defines one (R18). */
+enum { DMHA_SCORER_L2 = 0, DMHA_SCORER_PROJ = 1 };
+
+/* s_{psi,tau}: X_{L x D} -> X'_{L' x D}, PAPER.md Eq. `selector` P:630-634:
+ * "filtering tokens before computing attention", tau the pruning
+ * threshold.  On this rank's rows x (DEVICE [n_rows, width] bf16, row-major,
+ * 16-byte aligned, width % 8 == 0):
+ *   score_t = ||x_t||_2 (DMHA_SCORER_L2, psi = NULL) or |x_t . psi|
+ *   (DMHA_SCORER_PROJ, psi = DEVICE [width] bf16), accumulated in fp64;
+ *   keep x_t iff score_t >= tau, in original order.
+ * Never empty (R19): if no row on ANY rank passes, the highest-scoring row
+ * over all ranks (ties: smallest global position under the init layout, with
+ * L = n_rows * world_size) is kept by its owner.  Collective when
+ * world_size > 1 (all ranks call with the same n_rows, width, scorer, tau).
+ * Outputs: x_out DEVICE [n_rows, width] bf16 capacity — the first *n_kept
+ * rows are the kept rows; idx_out DEVICE [n_rows] int64 — the first *n_kept
+ * entries are their LOCAL row indices, increasing (the re-aggregation map,
+ * P:622); scores DEVICE [n_rows] fp64 or NULL; *n_kept HOST.  Synchronises
+ * the stream (n_kept is returned to the host).  bf16 dtype only.
+ * Errors: INVALID (null, sizes, alignment, scorer/psi mismatch, NaN tau),
+ * UNSUPPORTED (fp32 init dtype), STATE, OOM, CUDA, NCCL. */
+int dmha_select(const void *x, int64_t n_rows, int width, int scorer, const void *psi,
+                double tau, void *x_out, int64_t *idx_out, double *scores, int64_t *n_kept);
+
+/* Re-aggregation ("reordered and aggregated"): y_full[idx[i], :] =
+ * y_sel[i, :] for i < n_kept (DEVICE bf16 rows of `width`, 16-byte aligned;
+ * idx DEVICE int64 as returned by dmha_select); other rows untouched.
+ * Local (no collective).  Errors: INVALID, UNSUPPORTED (fp32), STATE, CUDA. */
+int dmha_scatter_rows(const void *y_sel, const int64_t *idx, int64_t n_kept, int width,
+                      void *y_full);
+
 /* Measurement hook: dev_buf (device, >= 4*9*64 uint64, or NULL to disable)
  * receives clock64 timeline stamps of the bf16 attention kernel (first 4 CTAs
  * of head 0, first 64 KV tiles; events documented in attn_fwd_sm100.cu). */

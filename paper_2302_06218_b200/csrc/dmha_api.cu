@@ -79,6 +79,8 @@ struct State {
   // NEXT-3 layer workspace (dmha_mha_forward): q, k, v, o, lse; cuBLAS handle
   void* mha = nullptr;
   size_t mha_bytes = 0;
+  void* sel = nullptr;  // NEXT-4 selector workspace
+  size_t sel_bytes = 0;
   cublasHandle_t blas = nullptr;
   // host-path staging
   void* st_qkv = nullptr;  // q, k, v back to back
@@ -161,7 +163,8 @@ void free_ptr(float*& p) {
 void update_ws_stat() {
   g.stats.workspace_bytes = 2 * g.kv_bytes + (g.acc_elems + g.part_elems) * 4 +
                             (g.lse_elems + g.part_lse_elems) * 4 +
-                            g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes + g.mha_bytes;
+                            g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes + g.mha_bytes +
+                            g.sel_bytes;
 }
 
 int alloc_or_oom(void** p, size_t bytes, const char* what) {
@@ -575,6 +578,7 @@ int dmha_finalize(void) {
   free_ptr(g.st_qkv);
   free_ptr(g.st_out);
   free_ptr(g.st_lse);
+  free_ptr(g.sel);
   free_ptr(g.hp);
   free_ptr(g.mha);
   if (g.blas) cublasDestroy(g.blas);
@@ -959,6 +963,116 @@ int dmha_attention_local(const void* q, const void* k, const void* v, void* out,
       return fail(DMHA_ERR_INVALID, "dmha_attention_local: pointers must be 16-byte aligned");
   dmha::PosMap qm{q_base0, q_base1, q_chunk}, km{k_base0, k_base1, k_chunk};
   return run_local(q, k, v, out, lse, Lq, Lk, D, H, causal ? 1 : 0, qm, km, out_mode);
+}
+
+// ---------------------------------------------------------------- NEXT-4
+// Token Selector s_{psi,tau} (PAPER.md Eq. `selector` P:630-634, readings
+// R18-R21): score, keep iff score >= tau in order, never empty over all ranks.
+int dmha_select(const void* x, int64_t n_rows, int width, int scorer, const void* psi,
+                double tau, void* x_out, int64_t* idx_out, double* scores, int64_t* n_kept) {
+  if (int rc = check_state()) return rc;
+  if (!x || !x_out || !idx_out || !n_kept) return fail(DMHA_ERR_INVALID, "dmha_select: null pointer");
+  if (n_rows < 1 || width < 8 || width % 8)
+    return fail(DMHA_ERR_INVALID, "dmha_select: need n_rows >= 1 and width a positive multiple of 8");
+  if (scorer != DMHA_SCORER_L2 && scorer != DMHA_SCORER_PROJ)
+    return fail(DMHA_ERR_INVALID, "dmha_select: unknown scorer %d", scorer);
+  if ((scorer == DMHA_SCORER_PROJ) != (psi != nullptr))
+    return fail(DMHA_ERR_INVALID, "dmha_select: psi must be given exactly for the projection scorer");
+  if (std::isnan(tau)) return fail(DMHA_ERR_INVALID, "dmha_select: tau is NaN");
+  auto mis = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+  if (mis(x) || mis(x_out) || (psi && mis(psi)) || (reinterpret_cast<uintptr_t>(idx_out) & 7))
+    return fail(DMHA_ERR_INVALID, "dmha_select: x/x_out/psi must be 16-byte aligned");
+  if (g.dtype != DMHA_BF16) return fail(DMHA_ERR_UNSUPPORTED, "dmha_select: bf16 rows only");
+  // workspace: flags | tile counts | tile offsets | 8 int64/double slots | scores
+  const int64_t nb = dmha::selector_tiles(n_rows);
+  const size_t off_counts = (static_cast<size_t>(n_rows) + 255) & ~size_t(255);
+  const size_t off_offsets = off_counts + ((static_cast<size_t>(nb) * 4 + 255) & ~size_t(255));
+  const size_t off_slots = off_offsets + static_cast<size_t>(nb) * 8;
+  const size_t off_scores = off_slots + 64;
+  const size_t need = off_scores + static_cast<size_t>(n_rows) * 8;
+  if (need > g.sel_bytes) {
+    free_ptr(g.sel);
+    g.sel_bytes = 0;
+    if (int rc = alloc_or_oom(&g.sel, need, "selector workspace")) return rc;
+    g.sel_bytes = need;
+    update_ws_stat();
+  }
+  char* ws = static_cast<char*>(g.sel);
+  auto* flags = reinterpret_cast<uint8_t*>(ws);
+  auto* counts = reinterpret_cast<int*>(ws + off_counts);
+  auto* offsets = reinterpret_cast<int64_t*>(ws + off_offsets);
+  auto* slots = reinterpret_cast<int64_t*>(ws + off_slots);  // [0] total [1] global [2] row [3] cand
+  auto* dbest = reinterpret_cast<double*>(slots + 4);         // [4] best score [5] global best
+  double* sc = scores ? scores : reinterpret_cast<double*>(ws + off_scores);
+  CK_LAUNCH(dmha::launch_selector_score(x, psi, n_rows, width, scorer, tau, sc, flags, counts,
+                                        g.stream));
+  CK_LAUNCH(dmha::launch_selector_scan(counts, n_rows, offsets, slots, g.stream));
+  g.stats.kernel_launches += 2;
+  if (g.world > 1) {
+    CK_NCCL(ncclAllReduce(slots, slots + 1, 1, ncclInt64, ncclSum, g.nccl, g.stream));
+  } else {
+    CK_CUDA(cudaMemcpyAsync(slots + 1, slots, 8, cudaMemcpyDeviceToDevice, g.stream));
+  }
+  int64_t h[2];
+  CK_CUDA(cudaMemcpyAsync(h, slots, 16, cudaMemcpyDeviceToHost, g.stream));
+  CK_CUDA(cudaStreamSynchronize(g.stream));
+  if (h[1] > 0) {  // something passes somewhere: plain order-preserving compaction
+    CK_LAUNCH(dmha::launch_selector_compact(x, n_rows, width, flags, offsets, x_out, idx_out,
+                                            g.stream));
+    g.stats.kernel_launches += 1;
+    *n_kept = h[0];
+    return DMHA_OK;
+  }
+  // Never-empty rule (R19): the highest score over all ranks, ties -> the
+  // smallest GLOBAL position, is kept by its owner.
+  CK_LAUNCH(dmha::launch_selector_argmax(sc, n_rows, dbest, slots + 2, g.stream));
+  g.stats.kernel_launches += 1;
+  if (g.world > 1) {
+    CK_NCCL(ncclAllReduce(dbest, dbest + 1, 1, ncclFloat64, ncclMax, g.nccl, g.stream));
+  } else {
+    CK_CUDA(cudaMemcpyAsync(dbest + 1, dbest, 8, cudaMemcpyDeviceToDevice, g.stream));
+  }
+  double hb[2];
+  int64_t hrow = 0;
+  CK_CUDA(cudaMemcpyAsync(hb, dbest, 16, cudaMemcpyDeviceToHost, g.stream));
+  CK_CUDA(cudaMemcpyAsync(&hrow, slots + 2, 8, cudaMemcpyDeviceToHost, g.stream));
+  CK_CUDA(cudaStreamSynchronize(g.stream));
+  const dmha::PosMap m = posmap(n_rows * g.world, g.world, g.rank, g.layout);
+  const int64_t my_gpos = hrow < m.chunk ? m.base0 + hrow : m.base1 + (hrow - m.chunk);
+  int64_t cand[2] = {hb[0] == hb[1] ? my_gpos : INT64_MAX, 0};
+  if (g.world > 1) {
+    CK_CUDA(cudaMemcpyAsync(slots + 3, cand, 8, cudaMemcpyHostToDevice, g.stream));
+    CK_NCCL(ncclAllReduce(slots + 3, slots + 1, 1, ncclInt64, ncclMin, g.nccl, g.stream));
+    CK_CUDA(cudaMemcpyAsync(cand + 1, slots + 1, 8, cudaMemcpyDeviceToHost, g.stream));
+    CK_CUDA(cudaStreamSynchronize(g.stream));
+  } else {
+    cand[1] = cand[0];
+  }
+  if (cand[0] != INT64_MAX && cand[0] == cand[1]) {
+    CK_CUDA(cudaMemcpyAsync(x_out, static_cast<const char*>(x) + hrow * width * 2,
+                            static_cast<size_t>(width) * 2, cudaMemcpyDeviceToDevice, g.stream));
+    CK_CUDA(cudaMemcpyAsync(idx_out, slots + 2, 8, cudaMemcpyDeviceToDevice, g.stream));
+    CK_CUDA(cudaStreamSynchronize(g.stream));
+    *n_kept = 1;
+  } else {
+    *n_kept = 0;
+  }
+  return DMHA_OK;
+}
+
+int dmha_scatter_rows(const void* y_sel, const int64_t* idx, int64_t n_kept, int width,
+                      void* y_full) {
+  if (int rc = check_state()) return rc;
+  if (n_kept < 0 || width < 8 || width % 8)
+    return fail(DMHA_ERR_INVALID, "dmha_scatter_rows: bad n_kept/width");
+  if (n_kept == 0) return DMHA_OK;
+  if (!y_sel || !idx || !y_full) return fail(DMHA_ERR_INVALID, "dmha_scatter_rows: null pointer");
+  auto mis = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+  if (mis(y_sel) || mis(y_full)) return fail(DMHA_ERR_INVALID, "dmha_scatter_rows: misaligned");
+  if (g.dtype != DMHA_BF16) return fail(DMHA_ERR_UNSUPPORTED, "dmha_scatter_rows: bf16 rows only");
+  CK_LAUNCH(dmha::launch_scatter_rows(y_sel, idx, n_kept, width, y_full, g.stream));
+  g.stats.kernel_launches += 1;
+  return DMHA_OK;
 }
 
 int dmha_lse_combine(float* o_acc, float* lse_acc, const float* o_part, const float* lse_part,

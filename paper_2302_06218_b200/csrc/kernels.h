@@ -69,6 +69,21 @@ cudaError_t launch_headpar_pack_out(const void* outg, void* send, const float* l
 cudaError_t launch_headpar_unpack_out(const void* recv, void* out, const HeadparGeom& g,
                                       int elem_bytes, cudaStream_t st);
 
+// Token Selector (selector.cu): 256-row tiles.
+int64_t selector_tiles(int64_t n);
+cudaError_t launch_selector_score(const void* x, const void* psi, int64_t n, int w, int scorer,
+                                  double tau, double* scores, uint8_t* flags, int* tile_counts,
+                                  cudaStream_t st);
+cudaError_t launch_selector_scan(const int* tile_counts, int64_t n, int64_t* offsets,
+                                 int64_t* total, cudaStream_t st);
+cudaError_t launch_selector_compact(const void* x, int64_t n, int w, const uint8_t* flags,
+                                    const int64_t* offsets, void* x_out, int64_t* idx_out,
+                                    cudaStream_t st);
+cudaError_t launch_selector_argmax(const double* scores, int64_t n, double* best,
+                                   int64_t* best_row, cudaStream_t st);
+cudaError_t launch_scatter_rows(const void* y_sel, const int64_t* idx, int64_t k, int w,
+                                void* y_full, cudaStream_t st);
+
 // Debug timeline buffer for the bf16 attention kernel (null = off).
 extern unsigned long long* g_trace;
 

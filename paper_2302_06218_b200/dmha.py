@@ -28,6 +28,7 @@ EXPORTED_SYMBOLS = (
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
     "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
     "dmha_forward_headpar", "dmha_forward_headpar_emulated", "dmha_mha_forward",
+    "dmha_select", "dmha_scatter_rows",
 )
 
 
@@ -87,6 +88,8 @@ def lib():
             "dmha_forward_headpar": [P, P, P, P, P, I64, I, I, I],
             "dmha_forward_headpar_emulated": [I, I, P, P, P, P, P, I64, I, I, I],
             "dmha_mha_forward": [P, P, P, P, P, P, P, I64, I, I, I, I],
+            "dmha_select": [P, I64, I, I, P, ctypes.c_double, P, P, P, ctypes.POINTER(I64)],
+            "dmha_scatter_rows": [P, P, I64, I, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -275,6 +278,37 @@ def lse_combine(o_acc, lse_acc, o_part, lse_part, out=None, lse_out=None, final:
     set_stream(_cur_stream())
     _check(lib().dmha_lse_combine(_ptr(o_acc), _ptr(lse_acc), _ptr(o_part), _ptr(lse_part),
                                   _ptr(out), _ptr(lse_out), Lq, D, H, int(bool(final))))
+
+
+SCORERS = {"l2": 0, "proj": 1}
+
+
+def select(x, tau: float, scorer: str = "l2", psi=None, x_out=None, idx_out=None, scores=None):
+    """NEXT-4 token Selector s_{psi,tau} (Eq. `selector`) on this rank's rows
+    x [n, width] (bf16 device tensor).  Returns (x_out[:n_kept] view,
+    idx_out[:n_kept] view of LOCAL row indices, scores [n] fp64)."""
+    import torch
+    n, w = x.shape
+    if x_out is None:
+        x_out = torch.empty_like(x)
+    if idx_out is None:
+        idx_out = torch.empty(n, dtype=torch.int64, device=x.device)
+    if scores is None:
+        scores = torch.empty(n, dtype=torch.float64, device=x.device)
+    k = ctypes.c_int64(0)
+    set_stream(_cur_stream())
+    _check(lib().dmha_select(_ptr(x), int(n), int(w), SCORERS[scorer], _ptr(psi), float(tau),
+                             _ptr(x_out), _ptr(idx_out), _ptr(scores), ctypes.byref(k)))
+    return x_out[:k.value], idx_out[:k.value], scores
+
+
+def scatter_rows(y_sel, idx, y_full):
+    """Re-aggregation (P:622): y_full[idx[i]] = y_sel[i] in place."""
+    k = int(idx.shape[0])
+    w = int(y_full.shape[1])
+    set_stream(_cur_stream())
+    _check(lib().dmha_scatter_rows(_ptr(y_sel), _ptr(idx), k, w, _ptr(y_full)))
+    return y_full
 
 
 def workspace_bytes(L: int, D: int, H: int) -> int:

@@ -96,6 +96,29 @@ def main():
         print(json.dumps(rec), flush=True)
         del oa, op, la, lp, out, lo
 
+    # NEXT-4 selector: X = C5's P=8 shard as rows of width H*D (131072 x 1024
+    # bf16, 256 MiB) and C4's P=1 (262144 x 2048), tau at the median score
+    res["selector"] = []
+    for n, w in ((131072, 1024), (262144, 2048)):
+        x = torch.randn(n, w, device="cuda").to(torch.bfloat16)
+        xo = torch.empty_like(x)
+        idx = torch.empty(n, dtype=torch.int64, device="cuda")
+        sc = torch.empty(n, dtype=torch.float64, device="cuda")
+        _, kept, _ = dmha.select(x, 0.0, "l2", None, xo, idx, sc)
+        tau = float(sc.median())
+        kept_n = [0]
+
+        def run():
+            kept_n[0] = dmha.select(x, tau, "l2", None, xo, idx, sc)[1].shape[0]
+        ms = time_cuda(run, iters=10)
+        k = kept_n[0]
+        by = n * w * 2 + 2 * k * w * 2 + 8 * n + n + 8 * k  # score read, row copy r+w, scores, flags, idx
+        rec = {"n": n, "width": w, "kept": k, "ms": ms, "gbs": by / ms / 1e6,
+               "frac_hbm": by / ms / 1e6 / PEAKS["hbm_gbs"], "note": "includes the host sync for n_kept"}
+        res["selector"].append(rec)
+        print(json.dumps(rec), flush=True)
+        del x, xo, idx, sc
+
     # whole per-rank ring compute through the emulation (C3 size P = 2, 4, 8;
     # C4 P = 8), with the NEXT-2 fused combine (default) and the separate pass
     cases = [(131072, 128, 8, P) for P in (2, 4, 8)] + [(262144, 128, 16, 8)]
