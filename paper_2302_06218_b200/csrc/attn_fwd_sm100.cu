@@ -673,13 +673,14 @@ int emu_variant() {
 }
 // Kernel choice: DMHA_KERNEL = pingpong | cluster | pair (default pingpong,
 // the measured fastest on C3/C4/C5).
-enum KernelKind { K_PINGPONG, K_CLUSTER, K_PAIR };
+enum KernelKind { K_PINGPONG, K_CLUSTER, K_PAIR, K_DBUF };
 inline KernelKind kernel_kind(int D) {
   const char* e = std::getenv("DMHA_KERNEL");
   if (e) {
     if (!strcmp(e, "pingpong")) return K_PINGPONG;
     if (!strcmp(e, "cluster")) return K_CLUSTER;
     if (!strcmp(e, "pair")) return D == 128 ? K_PAIR : K_CLUSTER;
+    if (!strcmp(e, "dbuf")) return K_DBUF;
   }
   return K_PINGPONG;
 }
@@ -749,7 +750,9 @@ unsigned long long* g_trace = nullptr;
 bool pingpong_fused_combine_ok();  // attn_fwd_sm100_v1.cu
 
 bool attn_fused_combine_supported(int D) {
-  return (D == 64 || D == 128) && kernel_kind(D) == K_PINGPONG && pingpong_fused_combine_ok();
+  if (D != 64 && D != 128) return false;
+  const KernelKind k = kernel_kind(D);
+  return k == K_DBUF || (k == K_PINGPONG && pingpong_fused_combine_ok());
 }
 
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream) {
@@ -758,6 +761,7 @@ cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   if (a.Lq > INT32_MAX || a.Lk > INT32_MAX) return cudaErrorInvalidValue;
   if (kernel_kind(a.D) == K_PINGPONG) return launch_attn_fwd_bf16_pingpong(a, stream);
+  if (kernel_kind(a.D) == K_DBUF) return launch_attn_fwd_bf16_dbuf(a, stream);
   if (a.D == 64) return launch_d<64>(a, stream);
   if (a.D == 128) return launch_d<128>(a, stream);
   return cudaErrorInvalidValue;

@@ -43,6 +43,8 @@ cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t s
 // Whether launch_attn_fwd_bf16 accepts OUT_COMBINE_* for head dim D (the
 // ping-pong kernel with the one-thread-per-row epilogue does).
 bool attn_fused_combine_supported(int D);
+// 64-key tiles with double-buffered scores (attn_fwd_sm100_v2.cu, "dbuf").
+cudaError_t launch_attn_fwd_bf16_dbuf(const LocalAttnArgs& a, cudaStream_t stream);
 // fp32 path (attn_fwd_fp32.cu).
 cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
 // log-sum-exp combine (lse_combine.cu).  out_dtype_bf16 selects the final

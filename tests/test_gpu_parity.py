@@ -234,7 +234,7 @@ def test_error_codes(lib_bf16):
     assert e.value.code == dmha.ERR_INVALID
 
 
-@pytest.mark.parametrize("kernel", ["pingpong", "cluster", "pair"])
+@pytest.mark.parametrize("kernel", ["pingpong", "cluster", "pair", "dbuf"])
 @pytest.mark.parametrize("L,H,D,causal", [(1000, 2, 128, False), (2085, 2, 64, True), (777, 3, 128, True),
                                           (4096, 1, 128, False), (300, 1, 64, False)])
 def test_kernel_variants_parity(lib_bf16, oracle_mod, monkeypatch, kernel, L, H, D, causal):
@@ -246,7 +246,7 @@ def test_kernel_variants_parity(lib_bf16, oracle_mod, monkeypatch, kernel, L, H,
     assert_parity(out, lse, ref_o, ref_l, "bf16", f"{kernel} L={L} H={H} D={D} causal={causal}")
 
 
-@pytest.mark.parametrize("kernel", ["pingpong", "cluster", "pair"])
+@pytest.mark.parametrize("kernel", ["pingpong", "cluster", "pair", "dbuf"])
 def test_kernel_variants_ring_partials(lib_bf16, oracle_mod, monkeypatch, kernel):
     """Variants on the ring path (global-position masks, fp32 partials, zigzag)."""
     monkeypatch.setenv("DMHA_KERNEL", kernel)
