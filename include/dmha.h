@@ -118,7 +118,12 @@ int dmha_forward(const void *q, const void *k, const void *v, void *out, float *
 
 /* Same operation with HOST buffers (pinned recommended): copies q/k/v to
  * device staging buffers, runs dmha_forward, copies out/lse back and
- * synchronises the stream before returning (the end-to-end path). */
+ * synchronises the stream before returning (the end-to-end path).  At world
+ * size 1 and L >= 65536 the copies are pipelined with the compute: the first
+ * Q row chunk (all of Q when causal) is attended over K/V blocks as they land
+ * (ring-style fused log-sum-exp combine); non-causal, the remaining Q chunks
+ * (up to 8) attend all keys as each lands, and each chunk's out/lse rows are
+ * copied back on a separate stream while the next one computes. */
 int dmha_forward_host(const void *q, const void *k, const void *v, void *out, float *lse,
                       int64_t L, int D, int H, int causal);
 

@@ -19,8 +19,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -66,6 +68,9 @@ struct State {
   ncclComm_t nccl = nullptr;
   cudaEvent_t ev_start = nullptr, ev_recv[2] = {nullptr, nullptr},
               ev_done[2] = {nullptr, nullptr}, ev_comm_end = nullptr;
+  // host path pipelining (dmha_forward_host at world size 1)
+  cudaStream_t d2h = nullptr;
+  cudaEvent_t ev_h2d[8] = {}, ev_comp[8] = {}, ev_kv[4] = {};
   // ring workspace
   void* kvbuf[2] = {nullptr, nullptr};  // each: K block then V block
   float* o_acc = nullptr;
@@ -590,6 +595,12 @@ int dmha_finalize(void) {
                         g.ev_done[1]};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 8; ++i) {
+    if (g.ev_h2d[i]) cudaEventDestroy(g.ev_h2d[i]);
+    if (g.ev_comp[i]) cudaEventDestroy(g.ev_comp[i]);
+    if (i < 4 && g.ev_kv[i]) cudaEventDestroy(g.ev_kv[i]);
+  }
+  if (g.d2h) cudaStreamDestroy(g.d2h);
   if (g.comm) cudaStreamDestroy(g.comm);
   g = State();
   return DMHA_OK;
@@ -737,6 +748,102 @@ int dmha_forward_host(const void* q, const void* k, const void* v, void* out, fl
   }
   update_ws_stat();
   char* dq = static_cast<char*>(g.st_qkv);
+  const char* pipe_env = std::getenv("DMHA_HOST_PIPELINE");  // 0: unpipelined (A/B knob)
+  if (g.world == 1 && L >= 2 * 32768 && !(pipe_env && std::atoi(pipe_env) == 0)) {
+    // Single GPU: pipeline the copies with the compute.  Q arrives in row
+    // chunks (non-causal) and K/V in key blocks, on a copy stream, in the order
+    //   Q chunk 0, K/V block 0, ..., K/V block 3, Q chunk 1, Q chunk 2, ...
+    // Chunk 0 is attended block by block as the K/V blocks land (the ring's
+    // fused log-sum-exp combine, bit-for-bit the combine the ring uses);
+    // later chunks attend all keys at once.  Each chunk's out/lse rows go back
+    // on a third stream while the next chunk computes.  Only Q chunk 0, the
+    // first K/V block and the last output chunk stay exposed.
+    if (D != 64 && D != 128)
+      return fail(DMHA_ERR_UNSUPPORTED, "dmha: per-head dim D=%d unsupported (64 or 128)", D);
+    if (!g.d2h) {
+      CK_CUDA(cudaStreamCreateWithFlags(&g.d2h, cudaStreamNonBlocking));
+      for (int i = 0; i < 8; ++i) {
+        CK_CUDA(cudaEventCreateWithFlags(&g.ev_h2d[i], cudaEventDisableTiming));
+        CK_CUDA(cudaEventCreateWithFlags(&g.ev_comp[i], cudaEventDisableTiming));
+        if (i < 4) CK_CUDA(cudaEventCreateWithFlags(&g.ev_kv[i], cudaEventDisableTiming));
+      }
+    }
+    causal = causal ? 1 : 0;
+    const size_t row_b = static_cast<size_t>(H) * D * elem_bytes(g.dtype);
+    // Causal: Q row chunks measured 4-8 % slower in the kernels (C5: 2830 ->
+    // 2950-3050 ms of attention), so causal runs split only the K/V copy.
+    int64_t nch = causal ? 1 : std::min<int64_t>(8, L / 32768);
+    if (const char* e = std::getenv("DMHA_HOST_CHUNKS")) nch = std::max<int64_t>(1, std::min<int64_t>(8, std::atoi(e)));
+    const int64_t per = ((L + nch - 1) / nch + 255) / 256 * 256;  // whole 256-row CTAs
+    int nkb = fused_combine(D) ? 4 : 1;                           // K/V blocks for chunk 0
+    if (const char* e = std::getenv("DMHA_HOST_KVBLOCKS")) nkb = std::max(1, std::min(nkb, std::atoi(e)));
+    const int64_t kper = (L + nkb - 1) / nkb;
+    const int64_t n0 = std::min<int64_t>(per, L);
+    if (nkb > 1)
+      if (int rc = ensure_ring_ws(n0, D, H, false)) return rc;
+    // staging buffers are free once earlier work on the compute stream is done
+    CK_CUDA(cudaEventRecord(g.ev_start, g.stream));
+    CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_start, 0));
+    CK_CUDA(cudaStreamWaitEvent(g.d2h, g.ev_start, 0));
+    auto h2d = [&](int64_t r0, int64_t n, size_t off, const void* src) {
+      return cudaMemcpyAsync(dq + off + r0 * row_b, static_cast<const char*>(src) + r0 * row_b,
+                             n * row_b, cudaMemcpyHostToDevice, g.comm);
+    };
+    CK_CUDA(h2d(0, n0, 0, q));
+    CK_CUDA(cudaEventRecord(g.ev_h2d[0], g.comm));
+    for (int b = 0; b < nkb; ++b) {
+      const int64_t k0 = b * kper, kn = std::min<int64_t>(kper, L - k0);
+      CK_CUDA(h2d(k0, kn, tb, k));
+      CK_CUDA(h2d(k0, kn, 2 * tb, v));
+      CK_CUDA(cudaEventRecord(g.ev_kv[b], g.comm));
+    }
+    int c = 1;
+    for (int64_t r0 = per; r0 < L; r0 += per, ++c) {
+      CK_CUDA(h2d(r0, std::min<int64_t>(per, L - r0), 0, q));
+      CK_CUDA(cudaEventRecord(g.ev_h2d[c], g.comm));
+    }
+    c = 0;
+    for (int64_t r0 = 0; r0 < L; r0 += per, ++c) {
+      const int64_t n = std::min<int64_t>(per, L - r0);
+      const dmha::PosMap qm{r0, r0 + n, n};
+      float* lse_c = g.st_lse + r0 * H;  // chunk-major [chunk][H][n]
+      char* out_c = static_cast<char*>(g.st_out) + r0 * row_b;
+      if (c == 0 && nkb > 1) {
+        for (int b = 0; b < nkb; ++b) {
+          const int64_t k0 = b * kper, kn = std::min<int64_t>(kper, L - k0);
+          CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_kv[b], 0));  // (Q chunk 0 precedes)
+          const dmha::PosMap km{k0, k0 + kn, kn};
+          const bool last = b == nkb - 1;
+          int rc = b == 0 ? run_local(dq, dq + tb, dq + 2 * tb, g.o_acc, g.lse_acc, n, kn, D, H,
+                                      causal, qm, km, dmha::OUT_PARTIAL_F32)
+                          : run_local(dq, dq + tb + k0 * row_b, dq + 2 * tb + k0 * row_b,
+                                      last ? static_cast<void*>(out_c) : g.o_acc,
+                                      last ? lse_c : g.lse_acc, n, kn, D, H, causal, qm, km,
+                                      last ? dmha::OUT_COMBINE_FINAL : dmha::OUT_COMBINE_ACC,
+                                      g.o_acc, g.lse_acc);
+          if (rc) return rc;
+        }
+      } else {
+        CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_h2d[c], 0));
+        CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_kv[nkb - 1], 0));
+        const dmha::PosMap km{0, L, L};
+        if (int rc = run_local(dq + r0 * row_b, dq + tb, dq + 2 * tb, out_c, lse_c, n, L, D, H,
+                               causal, qm, km, dmha::OUT_FINAL))
+          return rc;
+      }
+      CK_CUDA(cudaEventRecord(g.ev_comp[c], g.stream));
+      CK_CUDA(cudaStreamWaitEvent(g.d2h, g.ev_comp[c], 0));
+      CK_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + r0 * row_b, out_c, n * row_b,
+                              cudaMemcpyDeviceToHost, g.d2h));
+      CK_CUDA(cudaMemcpy2DAsync(lse + r0, static_cast<size_t>(L) * 4, lse_c,
+                                static_cast<size_t>(n) * 4, static_cast<size_t>(n) * 4, H,
+                                cudaMemcpyDeviceToHost, g.d2h));
+    }
+    CK_CUDA(cudaStreamSynchronize(g.d2h));
+    CK_CUDA(cudaStreamSynchronize(g.stream));
+    g.stats.forwards++;
+    return DMHA_OK;
+  }
   CK_CUDA(cudaMemcpyAsync(dq, q, tb, cudaMemcpyHostToDevice, g.stream));
   CK_CUDA(cudaMemcpyAsync(dq + tb, k, tb, cudaMemcpyHostToDevice, g.stream));
   CK_CUDA(cudaMemcpyAsync(dq + 2 * tb, v, tb, cudaMemcpyHostToDevice, g.stream));

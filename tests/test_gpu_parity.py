@@ -333,3 +333,26 @@ def test_fused_combine_bit_identical_to_separate_pass(lib_bf16, oracle_mod, monk
     ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
     assert_parity(out_g, lse_g, ref_o, ref_l, "bf16", f"fused ring P={P} {layout} causal={causal}")
 
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_host_path_pipelined(lib_bf16, oracle_mod, causal):
+    """dmha_forward_host at world size 1 and L >= 65536 pipelines the copies:
+    Q chunk 0 (all of Q when causal) is attended over K/V blocks as they land
+    (the ring's fused combine), later chunks over all keys.  Later chunks must
+    carry the bits of the device path; every sampled row must match the
+    oracle."""
+    L, H, D = 70000, 2, 64
+    q, k, v = inputs.qkv(L, H, D, seed=71)
+    a_o, a_l = run_p1(q, k, v, causal)
+    hq, hk, hv = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in (q, k, v))
+    ho, hl = dmha.forward_host(hq, hk, hv, L, causal)
+    ho = ho.float().numpy()
+    hl = hl.numpy()
+    half = L // 2 + 256  # past the first chunk (at most ceil(L/2) rounded up to 256 rows)
+    if not causal:  # causal runs split only the keys (all rows combined), see dmha.h
+        np.testing.assert_array_equal(ho[half:], a_o[half:])
+        np.testing.assert_array_equal(hl[:, half:], a_l[:, half:])
+    rows = _sample_rows(L, [17408, 35072, half], 128, seed=2)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal, rows=rows)
+    assert_parity(ho[rows], hl[:, rows], ref_o, ref_l, "bf16", f"host pipelined causal={causal}")
