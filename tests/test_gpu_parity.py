@@ -308,15 +308,17 @@ def test_mha_layer_matches_oracle(lib_bf16, oracle_mod, causal, D):
     assert np.max(np.abs(lse.cpu().numpy() - ref_l)) <= 2e-2
 
 
+@pytest.mark.parametrize("kernel", ["pingpong", "dbuf"])
 @pytest.mark.parametrize("P,layout,causal,D", [(2, "contiguous", False, 128), (4, "zigzag", True, 64),
                                                (8, "zigzag", True, 128), (3, "contiguous", True, 64)])
-def test_fused_combine_bit_identical_to_separate_pass(lib_bf16, oracle_mod, monkeypatch, P, layout,
-                                                      causal, D):
+def test_fused_combine_bit_identical_to_separate_pass(lib_bf16, oracle_mod, monkeypatch, kernel, P,
+                                                      layout, causal, D):
     """NEXT-2: the epilogue-fused LSE combine (default) gives exactly the bits
     of the separate lse_combine pass (shared combine_math.cuh, _rn arithmetic),
     and both match the oracle."""
     H = 2
     L = P * 777 if layout == "contiguous" else 2 * P * 389  # ragged shards
+    monkeypatch.setenv("DMHA_KERNEL", kernel)
     q, k, v = inputs.qkv(L, H, D, seed=900 + P)
     parts = [[dmha.shard(x, P, r, layout) for r in range(P)] for x in (q, k, v)]
     dq, dk, dv = (to_dev(np.stack(p)) for p in parts)
