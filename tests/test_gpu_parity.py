@@ -358,3 +358,17 @@ def test_host_path_pipelined(lib_bf16, oracle_mod, causal):
     rows = _sample_rows(L, [17408, 35072, half], 128, seed=2)
     ref_o, ref_l = oracle_mod.attention(q, k, v, causal, rows=rows)
     assert_parity(ho[rows], hl[:, rows], ref_o, ref_l, "bf16", f"host pipelined causal={causal}")
+
+
+@pytest.mark.parametrize("env", [{"DMHA_ISSUERS": "1"}, {"DMHA_ISSUERS": "2"}, {"DMHA_ISSUERS": "4"},
+                                 {"DMHA_EMU": "1"}, {"DMHA_EMU": "2"}, {"DMHA_SPLIT": "1"},
+                                 {"DMHA_KERNEL": "dbuf", "DMHA_DBUF_ALT": "1"}])
+@pytest.mark.parametrize("L,H,D,causal", [(777, 2, 64, True), (1000, 2, 128, False), (2085, 1, 64, False)])
+def test_measurement_knobs_keep_parity(lib_bf16, oracle_mod, monkeypatch, env, L, H, D, causal):
+    """Every kernel knob DESIGN.md reports a measurement for stays correct."""
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    q, k, v = inputs.qkv(L, H, D, seed=31 + L)
+    out, lse = run_p1(q, k, v, causal)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(out, lse, ref_o, ref_l, "bf16", f"{env} L={L} D={D} causal={causal}")

@@ -91,3 +91,35 @@ def test_select_errors():
     with pytest.raises(dmha.DmhaError) as e:
         dmha.select(x, 0.0, "proj", None)  # projection scorer needs psi
     assert e.value.code == dmha.ERR_INVALID
+
+
+def test_selector_attention_reaggregation_pipeline(oracle_mod):
+    """The proposed system's slice on one GPU: select tokens,
+    causal attention over the kept tokens only (kept order = original order,
+    so the causal mask over the selected sequence is the original one),
+    scatter the outputs back to the original positions.  Compared with the
+    oracle composition of the same three steps."""
+    L, H, D = 3000, 2, 64
+    q, k, v = inputs.qkv(L, H, D, seed=12)
+    x = q.reshape(L, H * D)  # score the tokens by their query rows
+    tau = float(np.quantile(osel.scores(x), 0.6)) * (1 + 1e-6)
+    dx = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    _, idx, _ = dmha.select(dx, tau)
+    sel = idx.cpu().numpy()
+    n = sel.size
+    dq, dk, dv = (torch.from_numpy(t).cuda().to(torch.bfloat16)[idx] for t in (q, k, v))
+    o, _ = dmha.forward(dq.contiguous(), dk.contiguous(), dv.contiguous(), n, True)
+    y = torch.zeros(L, H * D, dtype=torch.bfloat16, device="cuda")
+    dmha.scatter_rows(o.reshape(n, H * D).contiguous(), idx, y)
+    torch.cuda.synchronize()
+    _, ref_idx, _ = osel.select(x, tau)
+    np.testing.assert_array_equal(sel, ref_idx)
+    ref_o, _ = oracle_mod.attention(q[ref_idx], k[ref_idx], v[ref_idx], True)
+    ref_y = osel.scatter_rows(ref_o.reshape(n, H * D), ref_idx, np.zeros((L, H * D)))
+    got = y.float().cpu().numpy()
+    keep = np.zeros(L, bool)
+    keep[ref_idx] = True
+    assert np.all(got[~keep] == 0)
+    err = np.abs(got - ref_y).max()
+    rel = np.linalg.norm(got - ref_y) / np.linalg.norm(ref_y)
+    assert err <= 2e-2 and rel <= 5e-3, (err, rel)
