@@ -1,4 +1,4 @@
-// ex2_bf16.cu — throughput of ex2.approx.ftz.bf16x2 vs ex2.approx.ftz.f32 (exps/clk/SM).
+// ex2_bf16.cu — throughput of ex2.approx.ftz.bf16x2 / ex2.approx.f16x2 vs ex2.approx.ftz.f32 (exps/clk/SM).
 #include <cstdio>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -11,7 +11,8 @@ __global__ void k(float* out, int iters) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (MODE == 0) asm("ex2.approx.ftz.f32 %0, %0;" : "+f"(f[i]));
-      else asm("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(a[i]));
+      else if (MODE == 1) asm("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(a[i]));
+      else asm("ex2.approx.f16x2 %0, %0;" : "+r"(a[i]));
     }
   }
   long long t1 = clock64();
@@ -31,4 +32,11 @@ template <int MODE> void run(const char* name, float* d) {
     printf("%-22s warps/SM %2d: %.2f exps/clk/SM\n", name, warps, per * warps * 32 * iters * 16 / cyc);
   }
 }
-int main() { float* d; cudaMalloc(&d, 148 * 1024 * 4 + 148 * 4); run<0>("ex2.f32", d); run<1>("ex2.bf16x2", d); return 0; }
+int main() {
+  float* d;
+  cudaMalloc(&d, 148 * 1024 * 4 + 148 * 4);
+  run<0>("ex2.f32", d);
+  run<1>("ex2.bf16x2", d);
+  run<2>("ex2.f16x2", d);
+  return 0;
+}
