@@ -4,7 +4,8 @@
 
 Per local token the library needs (bf16):
   P = 1:  H*(8*D + 4) bytes       (q, k, v, out + lse; no workspace)
-  P > 1:  H*(24*D + 12) bytes     (+ two K/V ring buffers, fp32 O_acc/O_part, lse x2)
+  P > 1:  H*(20*D + 8) bytes      (+ two K/V ring buffers, fp32 O_acc, lse_acc; the
+                                   combine is fused, NEXT-2 — H*(24*D + 12) without)
 so L_max(P) = P * floor(free_HBM / bytes_per_token) (rounded to 2P*256).
 
 On this single GPU the P = 1 bound is demonstrated, not only computed: q, k, v,
@@ -91,7 +92,7 @@ def run_family(D, H, causal, free_bytes, rows=256):
            "full_forward_tflops_extrapolated": flops / (full_ms / 1e3) / 1e12}
     cap = {}
     for P in (1, 2, 4, 8):
-        pt = H * (8 * D + 4) if P == 1 else H * (24 * D + 12)
+        pt = H * (8 * D + 4) if P == 1 else H * (20 * D + 8)
         lp = P * int(0.96 * free_bytes // pt)
         lp -= lp % (2 * P * 256)
         cap[str(P)] = lp
