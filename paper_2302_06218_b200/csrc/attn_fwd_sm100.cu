@@ -755,8 +755,14 @@ bool attn_fused_combine_supported(int D) {
   return k == K_DBUF || (k == K_PINGPONG && pingpong_fused_combine_ok());
 }
 
+bool attn_kv_split_supported(int D) {
+  return (D == 64 || D == 128) && kernel_kind(D) == K_PINGPONG && pingpong_fused_combine_ok();
+}
+
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream) {
   if (a.Lq <= 0) return cudaSuccess;
+  if (a.kv_split != 1 && (!attn_kv_split_supported(a.D) || a.out_mode != OUT_PARTIAL_F32))
+    return cudaErrorInvalidValue;
   if (a.out_mode >= OUT_COMBINE_ACC && !attn_fused_combine_supported(a.D))
     return cudaErrorInvalidValue;
   if (a.Lq > INT32_MAX || a.Lk > INT32_MAX) return cudaErrorInvalidValue;

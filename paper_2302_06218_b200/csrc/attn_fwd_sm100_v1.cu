@@ -88,6 +88,9 @@ struct Params {
   int out_mode;
   float* acc_o;    // OUT_COMBINE_*: running accumulator (read; ACC also writes it)
   float* acc_lse;
+  void* out2;      // kv_split = 2: the z = 1 CTAs' partial output / lse
+  float* lse2;
+  int kv_split;    // 1, or 2: blockIdx.z picks one half of each CTA's key tiles
   int n_mblk;
   unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
@@ -171,7 +174,15 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
   const int mblk = p.causal ? (p.n_mblk - 1 - static_cast<int>(blockIdx.x))
                             : static_cast<int>(blockIdx.x);
   const int64_t m0 = static_cast<int64_t>(mblk) * (2 * kBM);
-  const int nkv = num_kv_tiles(p, m0);
+  // Split-KV (small grids): CTA z of a split covers tiles [jt0, jt0 + nkv) of
+  // its row block's visible key tiles and writes an fp32 partial (out2/lse2
+  // for z = 1) that the log-sum-exp combine merges.
+  const int nkv_all = num_kv_tiles(p, m0);
+  const int kv_half = (nkv_all + p.kv_split - 1) / p.kv_split;
+  const int jt0 = min(nkv_all, static_cast<int>(blockIdx.z) * kv_half);
+  const int nkv = min(nkv_all, jt0 + kv_half) - jt0;
+  void* const out_ptr = blockIdx.z ? p.out2 : p.out;
+  float* const lse_ptr = blockIdx.z ? p.lse2 : p.lse;
 
   if (warp == kProducerWarp && lane == 0) {
     ptx::mbar_init(q_full, 1);
@@ -218,7 +229,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
           for (int pn = 0; pn < C::kPanels; ++pn)
             ptx::tma_load_3d(tm, &kv_full[stage], sKV + stage * C::kTileBytes + pn * C::kPanelBytes,
-                             pn * 64, head, j * kBN);
+                             pn * 64, head, (jt0 + j) * kBN);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -449,7 +460,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&s_free[g]);
       }
-      const int64_t tile_lim = klim - static_cast<int64_t>(j) * kBN;
+      const int64_t tile_lim = klim - static_cast<int64_t>(jt0 + j) * kBN;
       const bool masked = !__all_sync(0xffffffffu, tile_lim >= kBN);  // same in both halves
       if (masked) {
         const int64_t nv64 = tile_lim - h * 64;
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     const bool empty = !(l_tot > 0.f);
     const float inv_l = empty ? 0.f : 1.f / l_tot;
     if (row_ok && h == 0)
-      p.lse[static_cast<int64_t>(head) * p.Lq + row] =
+      lse_ptr[static_cast<int64_t>(head) * p.Lq + row] =
           empty ? -INFINITY : (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
     const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D) + h * (D / 2);
 #pragma unroll
@@ -520,13 +531,13 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       }
       if (row_ok) {
         if (p.out_mode == OUT_PARTIAL_F32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out_ptr) + obase + c * 32);
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             dst[e] = make_float4(__fmul_rn(o[4 * e], inv_l), __fmul_rn(o[4 * e + 1], inv_l),
                                  __fmul_rn(o[4 * e + 2], inv_l), __fmul_rn(o[4 * e + 3], inv_l));
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out_ptr) + obase +
                                                 c * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -573,7 +584,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         ptx::mbar_arrive(&s_free[g]);
       }
 
-      int64_t nv64 = klim - static_cast<int64_t>(j) * kBN;
+      int64_t nv64 = klim - static_cast<int64_t>(jt0 + j) * kBN;
       const int nvalid = nv64 < 0 ? 0 : (nv64 > kBN ? kBN : static_cast<int>(nv64));
       const bool masked = !__all_sync(0xffffffffu, nvalid >= kBN);
       if (masked) {
@@ -678,7 +689,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     if (fused && row_ok) merge_weights(p.acc_lse[li], lse_s, wa, wp, lnew);
     if (row_ok) {
       if (p.out_mode == OUT_COMBINE_ACC) p.acc_lse[li] = lnew;
-      else p.lse[li] = lnew;
+      else lse_ptr[li] = lnew;
     }
     const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D);
 #pragma unroll
@@ -707,7 +718,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           for (int e = 0; e < 8; ++e)
             acc[e] = make_float4(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]);
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out_ptr) + obase +
                                                 c * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -722,13 +733,13 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         }
       } else if (row_ok) {
         if (p.out_mode == OUT_PARTIAL_F32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out_ptr) + obase + c * 32);
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             dst[e] = make_float4(__fmul_rn(o[4 * e], inv_l), __fmul_rn(o[4 * e + 1], inv_l),
                                  __fmul_rn(o[4 * e + 2], inv_l), __fmul_rn(o[4 * e + 3], inv_l));
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase +
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out_ptr) + obase +
                                                 c * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -819,9 +830,12 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.out_mode = a.out_mode;
   p.acc_o = a.acc_o;
   p.acc_lse = a.acc_lse;
+  p.out2 = a.out2;
+  p.lse2 = a.lse2;
+  p.kv_split = a.kv_split == 2 ? 2 : 1;
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.trace = g_trace;
-  dim3 grid(p.n_mblk, a.H);
+  dim3 grid(p.n_mblk, a.H, p.kv_split);
   attn_fwd_sm100_kernel<D, E, S, I><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }

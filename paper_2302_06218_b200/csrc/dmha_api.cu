@@ -194,10 +194,10 @@ bool fused_combine(int D) {
 
 // Ring accumulators (always), the partial buffers (unfused combine only) and
 // the K/V ring buffers (need_kv).
-int ensure_ring_ws(int64_t Lloc, int D, int H, bool need_kv) {
+int ensure_ring_ws(int64_t Lloc, int D, int H, bool need_kv, bool force_part = false) {
   const size_t elems = static_cast<size_t>(Lloc) * H * D;
   const size_t lse = static_cast<size_t>(Lloc) * H;
-  const bool need_part = !fused_combine(D);
+  const bool need_part = force_part || !fused_combine(D);
   if (elems > g.acc_elems) {
     free_ptr(g.o_acc);
     g.acc_elems = 0;
@@ -307,10 +307,14 @@ int validate(const void* q, const void* k, const void* v, const void* out, const
 
 int run_local(const void* q, const void* k, const void* v, void* out, float* lse, int64_t Lq,
               int64_t Lk, int D, int H, int causal, dmha::PosMap qm, dmha::PosMap km,
-              int out_mode, float* acc_o = nullptr, float* acc_lse = nullptr) {
+              int out_mode, float* acc_o = nullptr, float* acc_lse = nullptr, int kv_split = 1,
+              void* out2 = nullptr, float* lse2 = nullptr) {
   dmha::LocalAttnArgs a;
   a.acc_o = acc_o;
   a.acc_lse = acc_lse;
+  a.kv_split = kv_split;
+  a.out2 = out2;
+  a.lse2 = lse2;
   a.q = q;
   a.k = k;
   a.v = v;
@@ -381,8 +385,22 @@ int ring_compute_step(int s, int P, int r, int layout, const void* q, const void
   const dmha_ring_plan pl = make_plan(P, r, s, layout, L);
   const dmha::PosMap qm{pl.q_base0, pl.q_base1, pl.q_chunk}, km{pl.k_base0, pl.k_base1, pl.k_chunk};
   switch (pl.output) {
-    case DMHA_PLAN_FINAL:
-      return run_local(q, ks, vs, out, lse, Lloc, Lloc, D, H, causal, qm, km, dmha::OUT_FINAL);
+    case DMHA_PLAN_FINAL: {
+      // Small grids (fewer than 4 waves of 256-row CTAs, e.g. C2) leave SMs
+      // idle in the last wave: split each row block's keys over two CTAs
+      // and merge the two fp32 partials with the log-sum-exp combine.
+      const int64_t ctas = (Lloc + 255) / 256 * H;
+      const char* e = std::getenv("DMHA_KV_SPLIT");
+      const bool split = g.dtype == DMHA_BF16 && ctas < 4 * 148 && Lloc >= 2048 &&
+                         !(e && std::atoi(e) == 0) && dmha::attn_kv_split_supported(D);
+      if (!split)
+        return run_local(q, ks, vs, out, lse, Lloc, Lloc, D, H, causal, qm, km, dmha::OUT_FINAL);
+      if (int rc = ensure_ring_ws(Lloc, D, H, false, true)) return rc;
+      if (int rc = run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
+                             dmha::OUT_PARTIAL_F32, nullptr, nullptr, 2, g.o_part, g.lse_part))
+        return rc;
+      return run_combine(g.o_part, g.lse_part, out, lse, Lloc, D, H, 1);
+    }
     case DMHA_PLAN_ACC:
       return run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
                        dmha::OUT_PARTIAL_F32);

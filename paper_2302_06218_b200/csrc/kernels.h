@@ -33,6 +33,12 @@ struct LocalAttnArgs {
   int out_mode;
   float* acc_o = nullptr;    // OUT_COMBINE_*: running O_acc [Lq, H, D] fp32
   float* acc_lse = nullptr;  // OUT_COMBINE_*: running lse_acc [H, Lq]
+  // Split-KV (ping-pong kernel, OUT_PARTIAL_F32 only): kv_split = 2 launches
+  // a second grid plane whose CTAs take the second half of each row block's
+  // key tiles and write their partial to out2 / lse2.
+  int kv_split = 1;
+  void* out2 = nullptr;
+  float* lse2 = nullptr;
 };
 
 // bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu): picks
@@ -43,6 +49,8 @@ cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t s
 // Whether launch_attn_fwd_bf16 accepts OUT_COMBINE_* for head dim D (the
 // ping-pong kernel with the one-thread-per-row epilogue does).
 bool attn_fused_combine_supported(int D);
+// Whether launch_attn_fwd_bf16 accepts kv_split = 2 for head dim D.
+bool attn_kv_split_supported(int D);
 // 64-key tiles with double-buffered scores (attn_fwd_sm100_v2.cu, "dbuf").
 cudaError_t launch_attn_fwd_bf16_dbuf(const LocalAttnArgs& a, cudaStream_t stream);
 // fp32 path (attn_fwd_fp32.cu).

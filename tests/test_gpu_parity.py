@@ -338,13 +338,14 @@ def test_fused_combine_bit_identical_to_separate_pass(lib_bf16, oracle_mod, monk
 
 
 @pytest.mark.parametrize("causal", [False, True])
-def test_host_path_pipelined(lib_bf16, oracle_mod, causal):
+def test_host_path_pipelined(lib_bf16, oracle_mod, monkeypatch, causal):
     """dmha_forward_host at world size 1 and L >= 65536 pipelines the copies:
     Q chunk 0 (all of Q when causal) is attended over K/V blocks as they land
     (the ring's fused combine), later chunks over all keys.  Later chunks must
     carry the bits of the device path; every sampled row must match the
     oracle."""
     L, H, D = 70000, 2, 64
+    monkeypatch.setenv("DMHA_KV_SPLIT", "0")  # compare with the one-launch device path
     q, k, v = inputs.qkv(L, H, D, seed=71)
     a_o, a_l = run_p1(q, k, v, causal)
     hq, hk, hv = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in (q, k, v))
@@ -372,3 +373,19 @@ def test_measurement_knobs_keep_parity(lib_bf16, oracle_mod, monkeypatch, env, L
     out, lse = run_p1(q, k, v, causal)
     ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
     assert_parity(out, lse, ref_o, ref_l, "bf16", f"{env} L={L} D={D} causal={causal}")
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("D", [64, 128])
+def test_kv_split_small_grid(lib_bf16, oracle_mod, monkeypatch, causal, D):
+    """Small grids split each row block's keys over two CTAs and merge the fp32
+    partials (log-sum-exp combine); the result matches the oracle and, within
+    the tolerance, the unsplit launch."""
+    L, H = 5000, 3
+    q, k, v = inputs.qkv(L, H, D, seed=41 + D)
+    a_o, a_l = run_p1(q, k, v, causal)  # split (L*H small)
+    monkeypatch.setenv("DMHA_KV_SPLIT", "0")
+    b_o, b_l = run_p1(q, k, v, causal)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(a_o, a_l, ref_o, ref_l, "bf16", f"kv split D={D} causal={causal}")
+    assert_parity(b_o, b_l, ref_o, ref_l, "bf16", f"unsplit D={D} causal={causal}")
