@@ -101,3 +101,55 @@ def test_c5_ring_p8_zigzag_causal(oracle_mod):
     chunk = L // (2 * P)
     rows = _rows(L, [c * chunk for c in range(1, 2 * P)], 16, 96, seed=5)
     _check(out, lse, q, k, v, True, rows, oracle_mod, "C5 ring P=8 zigzag")
+
+
+def test_64bit_offsets_large_q(oracle_mod):
+    """Output offsets beyond 2^31 elements: 4.2 M query rows x 16 heads x 64
+    (4.3e9 elements) against 128 keys; sampled rows (incl. the last ones)
+    against the oracle."""
+    Lq, Lk, H, D = (1 << 22) + 200, 128, 16, 64
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn((Lq, H, D), generator=gen, device="cuda").to(torch.bfloat16)
+    k, v = (torch.randn((Lk, H, D), generator=gen, device="cuda").to(torch.bfloat16) for _ in range(2))
+    out = torch.empty_like(q)
+    lse = torch.empty((H, Lq), dtype=torch.float32, device="cuda")
+    dmha.attention_local(q, k, v, out, lse)
+    torch.cuda.synchronize()
+    rows = torch.tensor(sorted({0, 1, 12345, (1 << 21) + 7, (1 << 22) - 1, Lq - 2, Lq - 1}), device="cuda")
+    qs = q[rows].float().cpu().numpy()
+    kk, vv = k.float().cpu().numpy(), v.float().cpu().numpy()
+    # the oracle on (sampled rows, all 128 keys): rows become a [n, H, D] query block
+    ref_o = np.empty((len(rows), H, D))
+    ref_l = np.empty((H, len(rows)))
+    for i in range(len(rows)):
+        qi = np.concatenate([qs[i:i + 1], np.zeros((Lk - 1, H, D), np.float32)])
+        o_i, l_i = oracle_mod.attention(qi, kk, vv, False, rows=np.array([0]))
+        ref_o[i], ref_l[:, i] = o_i[0], l_i[:, 0]
+    got_o = out[rows].float().cpu().numpy()
+    got_l = lse[:, rows].cpu().numpy()
+    assert_parity(got_o, got_l, ref_o, ref_l, "bf16", "64-bit output offsets")
+
+
+def test_64bit_offsets_large_kv():
+    """K/V offsets beyond 2^31 elements: 256 zero queries at the end of a
+    4.2 M-row sequence against all 4.2 M keys x 16 heads x 64: the closed form
+    (Q = 0) is out = mean of V per head, lse = ln L."""
+    L, H, D = (1 << 22) + 384, 16, 64
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    k = torch.randn((L, H, D), generator=gen, device="cuda").to(torch.bfloat16)
+    # V ramps with the row index (plus noise), so reading the wrong rows (e.g.
+    # a wrapped 32-bit offset) moves the mean far outside the tolerance
+    ramp = (torch.arange(L, device="cuda", dtype=torch.float32) / L)[:, None, None]
+    v = (ramp + 0.1 * torch.randn((L, H, D), generator=gen, device="cuda")).to(torch.bfloat16)
+    q = torch.zeros((256, H, D), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(q)
+    lse = torch.empty((H, 256), dtype=torch.float32, device="cuda")
+    dmha.attention_local(q, k, v, out, lse, qmap=(L - 256, L, 256))
+    torch.cuda.synchronize()
+    mean_v = v.double().mean(dim=0)  # [H, D]
+    err = (out.double() - mean_v[None]).abs().max().item()
+    # north_star max-abs bound; the error here is the fp32 tensor-core
+    # accumulation of 4.2 M all-positive terms (uniform attention, sum ~ 2e6),
+    # measured 8e-3.  Wrong rows would move the mean by > 0.1.
+    assert err <= 2e-2, err
+    assert np.allclose(lse.cpu().numpy(), np.log(L), atol=1e-3)
