@@ -292,13 +292,24 @@ def run_ours(args, w):
         except Exception:
             traffic = None
     attn_share = st1["attn_ms"] / args.steps / step_ms_local if step_ms_local > 0 else None
-    roofline = {"bound": "tensor", "kernel": f"attn_fwd_sm100_kernel<{D}>", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_kind": f"bf16 dense sustained, {peak_src}",
-                "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
-                "frac_of_datasheet_2250": achieved / 2250.0,
-                "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
-                "share_of_step": attn_share}
+    if w["dtype"] == "fp32":
+        # SIMT fp32 kernel: bound by the FP32 FMA pipe, 148 SMs x 128 lanes x
+        # 2 FLOP per clock at the maximum SM clock (DESIGN.md §5 fp32 path)
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        roofline = {"bound": "alu", "kernel": f"attn_fwd_fp32_kernel<{D}>", "achieved": achieved,
+                    "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                    "peak_kind": f"FP32 FMA pipe, 148x128x2 FLOP/clk at {sm_mhz:.0f} MHz (derived)",
+                    "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
+                    "share_of_step": attn_share}
+    else:
+        roofline = {"bound": "tensor", "kernel": f"attn_fwd_sm100_kernel<{D}>", "achieved": achieved,
+                    "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                    "peak_kind": f"bf16 dense sustained, {peak_src}",
+                    "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
+                    "frac_of_datasheet_2250": achieved / 2250.0,
+                    "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
+                    "share_of_step": attn_share}
     secondary = {}
     if st1["combine_launches"]:
         cm = st1["combine_ms"] / st1["combine_launches"]
