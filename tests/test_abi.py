@@ -101,3 +101,29 @@ def test_bad_layout_args():
         dmha.local_to_global(12, 4, 0, "zigzag", 0)       # 12 % 8 != 0
     with pytest.raises(dmha.DmhaError):
         dmha.local_to_global(16, 4, 4, "zigzag", 0)       # rank out of range
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No fallback: without libdmha.so every call raises DmhaError (the
+    product never routes through the oracle or a CPU path)."""
+    from paper_2302_06218_b200 import dmha
+    monkeypatch.setattr(dmha, "_lib", None)
+    monkeypatch.setattr(dmha, "_LIB_PATH", tmp_path / "libdmha.so")
+    with pytest.raises(dmha.DmhaError):
+        dmha.lib()
+    with pytest.raises(dmha.DmhaError):
+        dmha.workspace_bytes(1024, 64, 2)
+
+
+def test_product_does_not_import_the_oracle():
+    """The product package (binding and CUDA sources) never imports, links or
+    includes anything under oracle/ (comments may mention it)."""
+    import pathlib
+    import re
+    root = pathlib.Path(__file__).resolve().parent.parent / "paper_2302_06218_b200"
+    pat = re.compile(r"^\s*(from\s+oracle|import\s+oracle|#\s*include\s*[<\"].*oracle)", re.M)
+    files = list(root.glob("*.py")) + [f for f in (root / "csrc").glob("*") if f.is_file()]
+    assert files
+    for f in files:
+        assert not pat.search(f.read_text(errors="ignore")), f
+    assert "oracle" not in (root / "build.py").read_text()
