@@ -747,16 +747,16 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
 
 unsigned long long* g_trace = nullptr;
 
-bool pingpong_fused_combine_ok();  // attn_fwd_sm100_v1.cu
+bool pingpong_fused_combine_ok(int D);  // attn_fwd_sm100_v1.cu
 
 bool attn_fused_combine_supported(int D) {
   if (D != 64 && D != 128) return false;
   const KernelKind k = kernel_kind(D);
-  return k == K_DBUF || (k == K_PINGPONG && pingpong_fused_combine_ok());
+  return k == K_DBUF || (k == K_PINGPONG && pingpong_fused_combine_ok(D));
 }
 
 bool attn_kv_split_supported(int D) {
-  return (D == 64 || D == 128) && kernel_kind(D) == K_PINGPONG && pingpong_fused_combine_ok();
+  return (D == 64 || D == 128) && kernel_kind(D) == K_PINGPONG && pingpong_fused_combine_ok(D);
 }
 
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream) {

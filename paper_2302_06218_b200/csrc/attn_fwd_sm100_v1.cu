@@ -482,14 +482,18 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         l_run *= alpha;
         m_run = m_new;
       }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       if constexpr (kSepP) {
+        // exponentials first, then wait for PV_g(j-1) to have read P_g(j-1)
+        sm::exp_inplace64(s, sl2, m_use);
         if (j > 0) {
           ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
           ptx::tc_fence_after();
         }
+        l_run += sm::store_p64(s, tP);
+      } else {
+        l_run += sm::exp_half(s, sl2, m_use, tP);
       }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      l_run += sm::exp_half(s, sl2, m_use, tP);
       if (warp_rescale && j > 0) {  // this half's D/2 columns of O
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -510,14 +514,22 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       ptx::mbar_wait(&o_final[g], 0);
       ptx::tc_fence_after();
     }
+    const int64_t li = static_cast<int64_t>(head) * p.Lq + row;
+    const bool fused = p.out_mode >= OUT_COMBINE_ACC;
+    // both halves read lse_acc before the barrier; h = 0 writes it after
+    const float la = (fused && row_ok) ? p.acc_lse[li] : 0.f;
     redl[(g * 2 + h) * kBM + r] = l_run;
     asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
     const float l_tot = l_run + redl[(g * 2 + (h ^ 1)) * kBM + r];
     const bool empty = !(l_tot > 0.f);
     const float inv_l = empty ? 0.f : 1.f / l_tot;
-    if (row_ok && h == 0)
-      lse_ptr[static_cast<int64_t>(head) * p.Lq + row] =
-          empty ? -INFINITY : (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
+    const float lse_s = empty ? -INFINITY : (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
+    float wa = 0.f, wp = 0.f, lnew = lse_s;
+    if (fused && row_ok) merge_weights(la, lse_s, wa, wp, lnew);
+    if (row_ok && h == 0) {
+      if (p.out_mode == OUT_COMBINE_ACC) p.acc_lse[li] = lnew;
+      else lse_ptr[li] = lnew;
+    }
     const int64_t obase = (row * p.H + head) * static_cast<int64_t>(D) + h * (D / 2);
 #pragma unroll
     for (int c = 0; c < D / 64; ++c) {
@@ -529,7 +541,36 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = 0.f;
       }
-      if (row_ok) {
+      if (row_ok && fused) {
+        float4* acc = reinterpret_cast<float4*>(p.acc_o + obase + c * 32);
+        float rr[32];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float4 a4 = acc[e];
+          rr[4 * e + 0] = combine_one(a4.x, __fmul_rn(o[4 * e + 0], inv_l), wa, wp);
+          rr[4 * e + 1] = combine_one(a4.y, __fmul_rn(o[4 * e + 1], inv_l), wa, wp);
+          rr[4 * e + 2] = combine_one(a4.z, __fmul_rn(o[4 * e + 2], inv_l), wa, wp);
+          rr[4 * e + 3] = combine_one(a4.w, __fmul_rn(o[4 * e + 3], inv_l), wa, wp);
+        }
+        if (p.out_mode == OUT_COMBINE_ACC) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            acc[e] = make_float4(rr[4 * e], rr[4 * e + 1], rr[4 * e + 2], rr[4 * e + 3]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out_ptr) + obase +
+                                                c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t wd[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(rr[8 * e + 2 * t], rr[8 * e + 2 * t + 1]);
+              wd[t] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[e] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+          }
+        }
+      } else if (row_ok) {
         if (p.out_mode == OUT_PARTIAL_F32) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out_ptr) + obase + c * 32);
 #pragma unroll
@@ -854,9 +895,12 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   if (const char* e = std::getenv("DMHA_EMU")) emu = std::atoi(e);
   int iss = D == 64 ? 3 : 1;
   if (const char* e = std::getenv("DMHA_ISSUERS")) iss = std::atoi(e);
-  bool split = false;
+  // D = 64 default: the split softmax (16 softmax warps, two per row) with
+  // split QK^T / PV issuers (DESIGN.md §5 lesson 16); DMHA_SPLIT=0|1 overrides.
+  bool split = (D == 64);
   if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
   if (split) {
+    if (D == 64 && iss == 3) return launch_de<D, 0, true, 3>(a, stream);
     if (a.out_mode >= OUT_COMBINE_ACC) return cudaErrorInvalidValue;  // see pingpong_fused_combine_ok
     return launch_de<D, 0, true, 1>(a, stream);
   }
@@ -882,9 +926,15 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
 
 // The fused combine lives in the one-thread-per-row epilogue; the split
 // softmax (two threads per row, DMHA_SPLIT=1) keeps the separate combine.
-bool pingpong_fused_combine_ok() {
-  const char* e = std::getenv("DMHA_SPLIT");
-  return !(e && std::atoi(e) != 0);
+bool pingpong_fused_combine_ok(int D) {
+  // The one-thread-per-row epilogue merges; so does the split softmax's when
+  // it runs with split issuers (the D = 64 default).  Other split
+  // configurations keep the separate combine pass.
+  bool split = (D == 64);
+  if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
+  int iss = D == 64 ? 3 : 1;
+  if (const char* e = std::getenv("DMHA_ISSUERS")) iss = std::atoi(e);
+  return !split || (D == 64 && iss == 3);
 }
 
 cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t stream) {

@@ -173,6 +173,36 @@ __device__ __forceinline__ float store_p(const float (&s)[128], uint32_t tP) {
   return t.x + t.y;
 }
 
+// Half-row versions (64 columns, split softmax): exponentials in place, then
+// pack + store 32 P columns at tP and return the fp32 sum.
+__device__ __forceinline__ void exp_inplace64(float (&s)[64], float sl2, float m_use) {
+  const float2 sc2 = make_float2(sl2, sl2);
+  const float2 nm2 = make_float2(-m_use, -m_use);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+    s[2 * i] = ptx::ex2_approx(x.x);
+    s[2 * i + 1] = ptx::ex2_approx(x.y);
+  }
+}
+__device__ __forceinline__ float store_p64(const float (&s)[64], uint32_t tP) {
+  float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float2 pe = make_float2(s[32 * c + 2 * e], s[32 * c + 2 * e + 1]);
+      acc[e & 1] = __fadd2_rn(acc[e & 1], pe);
+      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
+      pk[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    ptx::tmem_st16(tP + c * 16, pk);
+  }
+  const float2 t = __fadd2_rn(acc[0], acc[1]);
+  return t.x + t.y;
+}
+
 // Row max of 128 scores as a shallow tree: 16 independent 3-input max chains
 // of depth 4, then a 3-level tree (instead of 4 serial chains of depth 32).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
