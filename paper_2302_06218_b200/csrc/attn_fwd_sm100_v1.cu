@@ -485,7 +485,10 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       if constexpr (kSepP) {
         // exponentials first, then wait for PV_g(j-1) to have read P_g(j-1)
-        sm::exp_inplace64(s, sl2, m_use);
+        if (kEmu == 0 || masked)
+          sm::exp_inplace64<0>(s, sl2, m_use);
+        else
+          sm::exp_inplace64<(kEmu > 4 ? 4 : kEmu)>(s, sl2, m_use);
         if (j > 0) {
           ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
           ptx::tc_fence_after();
@@ -900,7 +903,13 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   bool split = (D == 64);
   if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
   if (split) {
-    if (D == 64 && iss == 3) return launch_de<D, 0, true, 3>(a, stream);
+    if (D == 64 && iss == 3) {
+      switch (emu) {
+        case 1: return launch_de<D, 1, true, 3>(a, stream);
+        case 2: return launch_de<D, 2, true, 3>(a, stream);
+        default: return launch_de<D, 0, true, 3>(a, stream);
+      }
+    }
     if (a.out_mode >= OUT_COMBINE_ACC) return cudaErrorInvalidValue;  // see pingpong_fused_combine_ok
     return launch_de<D, 0, true, 1>(a, stream);
   }

@@ -175,14 +175,16 @@ __device__ __forceinline__ float store_p(const float (&s)[128], uint32_t tP) {
 
 // Half-row versions (64 columns, split softmax): exponentials in place, then
 // pack + store 32 P columns at tP and return the fp32 sum.
+template <int EMU = 0>  // EMU of every 8 column pairs on the FMA-pipe polynomial (finite inputs)
 __device__ __forceinline__ void exp_inplace64(float (&s)[64], float sl2, float m_use) {
   const float2 sc2 = make_float2(sl2, sl2);
   const float2 nm2 = make_float2(-m_use, -m_use);
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
-    s[2 * i] = ptx::ex2_approx(x.x);
-    s[2 * i + 1] = ptx::ex2_approx(x.y);
+    const float2 pe = ((i & 7) < EMU) ? exp2_poly2(x) : exp2_mufu2(x);
+    s[2 * i] = pe.x;
+    s[2 * i + 1] = pe.y;
   }
 }
 __device__ __forceinline__ float store_p64(const float (&s)[64], uint32_t tP) {
