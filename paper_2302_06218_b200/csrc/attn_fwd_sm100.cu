@@ -46,6 +46,7 @@
 #include <cstring>
 
 #include "kernels.h"
+#include "tma_map.h"
 #include "ptx_sm100.cuh"
 #include "softmax_sm100.cuh"
 
@@ -623,43 +624,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return nullptr;
-    fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  }
-  return fn;
-}
-
-// [L, H, D] bf16 viewed as a 3-D tensor (D, H, L); box (64, 1, box_rows), 128B swizzle.
-bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D, int box_rows) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  // A zero-length block is never loaded (no KV tiles) but the map must be valid.
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(H),
-                        static_cast<cuuint64_t>(L > 0 ? L : 1)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2,
-                           static_cast<cuuint64_t>(D) * H * 2};
-  cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // Kernel variant (measurement knobs): DMHA_EMU=<pairs of 8 on the FMA pipe>,
 // DMHA_PAIR_MMA=0 to use the per-CTA MMA path for D = 128.
 template <int D>
@@ -689,13 +653,16 @@ template <int D, int E, bool K2>
 cudaError_t launch_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const Params& p, dim3 grid, cudaStream_t stream) {
   using C = Cfg<D, K2>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the dynamic shared-memory limit is a per-device function attribute
+  static int attr_dev = -1;
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  if (attr_dev != cur_dev) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, K2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_dev = cur_dev;
   }
   attn_fwd_sm100_kernel<D, E, K2><<<grid, kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
@@ -720,8 +687,8 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   CUtensorMap tq, tk, tv;
   // K: 64-key half tiles (pair MMA: own half; multicast path: half per CTA).
   // V: pair MMA loads all 128 keys x 64 columns; multicast path 64-key halves.
-  if (!make_map(&tq, a.q, a.Lq, a.H, D, kBM) || !make_map(&tk, a.k, a.Lk, a.H, D, kBN / 2) ||
-      !make_map(&tv, a.v, a.Lk, a.H, D, k2 ? kBN : kBN / 2))
+  if (!make_tma_map_bf16(&tq, a.q, a.Lq, a.H, D, kBM) || !make_tma_map_bf16(&tk, a.k, a.Lk, a.H, D, kBN / 2) ||
+      !make_tma_map_bf16(&tv, a.v, a.Lk, a.H, D, k2 ? kBN : kBN / 2))
     return cudaErrorInvalidValue;
   Params p;
   p.Lq = a.Lq;

@@ -42,6 +42,7 @@
 
 #include "combine_math.cuh"
 #include "kernels.h"
+#include "tma_map.h"
 #include "ptx_sm100.cuh"
 #include "softmax_sm100.cuh"
 
@@ -809,57 +810,23 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return nullptr;
-    fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  }
-  return fn;
-}
-
-// [L, H, D] bf16 viewed as a 3-D tensor (D, H, L); box (64, 1, 128), 128B swizzle.
-bool make_map(CUtensorMap* map, const void* base, int64_t L, int H, int D) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  // A zero-length block is never loaded (nkv = 0) but the map must be valid.
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(H),
-                        static_cast<cuuint64_t>(L > 0 ? L : 1)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2,
-                           static_cast<cuuint64_t>(D) * H * 2};
-  cuuint32_t box[3] = {64, 1, 128};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 template <int D, int E, bool S, int I = 2>
 cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   using C = Cfg<D>;
   CUtensorMap tq, tk, tv;
-  if (!make_map(&tq, a.q, a.Lq, a.H, D) || !make_map(&tk, a.k, a.Lk, a.H, D) ||
-      !make_map(&tv, a.v, a.Lk, a.H, D))
+  if (!make_tma_map_bf16(&tq, a.q, a.Lq, a.H, D, kBM) || !make_tma_map_bf16(&tk, a.k, a.Lk, a.H, D, kBN) ||
+      !make_tma_map_bf16(&tv, a.v, a.Lk, a.H, D, kBN))
     return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the dynamic shared-memory limit is a per-device function attribute
+  static int attr_dev = -1;
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  if (attr_dev != cur_dev) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, S, I>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_dev = cur_dev;
   }
   Params p;
   p.Lq = a.Lq;
