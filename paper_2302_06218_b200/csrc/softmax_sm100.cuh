@@ -1,7 +1,8 @@
 // softmax_sm100.cuh — exponential helpers shared by the attention kernels:
 // P = exp2(S*scale*log2e - m) for one 128-column score row per thread, on
 // MUFU.EX2 or (for EMU of every 8 column pairs) on the FMA pipe, packed to bf16
-// and stored to TMEM.
+// and stored to TMEM — the numerator of the row softmax of PAPER.md:198-201
+// (online form with a running max m, readings R11/R16).
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
