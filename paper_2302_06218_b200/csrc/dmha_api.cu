@@ -70,7 +70,7 @@ struct State {
               ev_done[2] = {nullptr, nullptr}, ev_comm_end = nullptr;
   // host path pipelining (dmha_forward_host at world size 1)
   cudaStream_t d2h = nullptr;
-  cudaEvent_t ev_h2d[8] = {}, ev_comp[8] = {}, ev_kv[4] = {};
+  cudaEvent_t ev_h2d[8] = {}, ev_comp[8] = {}, ev_kv[8] = {};
   // ring workspace
   void* kvbuf[2] = {nullptr, nullptr};  // each: K block then V block
   float* o_acc = nullptr;
@@ -616,7 +616,7 @@ int dmha_finalize(void) {
   for (int i = 0; i < 8; ++i) {
     if (g.ev_h2d[i]) cudaEventDestroy(g.ev_h2d[i]);
     if (g.ev_comp[i]) cudaEventDestroy(g.ev_comp[i]);
-    if (i < 4 && g.ev_kv[i]) cudaEventDestroy(g.ev_kv[i]);
+    if (g.ev_kv[i]) cudaEventDestroy(g.ev_kv[i]);
   }
   if (g.d2h) cudaStreamDestroy(g.d2h);
   if (g.comm) cudaStreamDestroy(g.comm);
@@ -783,7 +783,7 @@ int dmha_forward_host(const void* q, const void* k, const void* v, void* out, fl
       for (int i = 0; i < 8; ++i) {
         CK_CUDA(cudaEventCreateWithFlags(&g.ev_h2d[i], cudaEventDisableTiming));
         CK_CUDA(cudaEventCreateWithFlags(&g.ev_comp[i], cudaEventDisableTiming));
-        if (i < 4) CK_CUDA(cudaEventCreateWithFlags(&g.ev_kv[i], cudaEventDisableTiming));
+        CK_CUDA(cudaEventCreateWithFlags(&g.ev_kv[i], cudaEventDisableTiming));
       }
     }
     causal = causal ? 1 : 0;
@@ -793,7 +793,7 @@ int dmha_forward_host(const void* q, const void* k, const void* v, void* out, fl
     int64_t nch = causal ? 1 : std::min<int64_t>(8, L / 32768);
     if (const char* e = std::getenv("DMHA_HOST_CHUNKS")) nch = std::max<int64_t>(1, std::min<int64_t>(8, std::atoi(e)));
     const int64_t per = ((L + nch - 1) / nch + 255) / 256 * 256;  // whole 256-row CTAs
-    int nkb = fused_combine(D) ? 4 : 1;                           // K/V blocks for chunk 0
+    int nkb = fused_combine(D) ? 8 : 1;                           // K/V blocks for chunk 0
     if (const char* e = std::getenv("DMHA_HOST_KVBLOCKS")) nkb = std::max(1, std::min(nkb, std::atoi(e)));
     const int64_t kper = (L + nkb - 1) / nkb;
     const int64_t n0 = std::min<int64_t>(per, L);
