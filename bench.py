@@ -310,6 +310,15 @@ def run_ours(args, w):
                     "frac_of_datasheet_2250": achieved / 2250.0,
                     "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
                     "share_of_step": attn_share}
+        if D == 64:
+            # At D = 64 one exponential (MUFU, 16/clk/SM) per score binds before
+            # the tensor pipe: ceiling = 148 SMs x 16 x 4*D FLOP per clock
+            # (DESIGN.md §5 a2), at the maximum and at the measured SM clock.
+            mx = float(peaks.get("sm_max_mhz", 1965.0))
+            roofline["exp_ceiling"] = {
+                "peak_at_max_clock": 148 * 16 * 4 * D * mx * 1e6 / 1e12,
+                "frac_at_max_clock": achieved / (148 * 16 * 4 * D * mx * 1e6 / 1e12),
+                "unit": "TFLOP/s", "pipe": "MUFU ex2, 16/clk/SM (measured, tools/mufu_rate.cu)"}
     secondary = {}
     if st1["combine_launches"]:
         cm = st1["combine_ms"] / st1["combine_launches"]
