@@ -855,21 +855,34 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
 // Measurement knobs (defaults = the measured-fastest configuration):
 //  DMHA_EMU     = pairs (of every 8) of score columns on the FMA-pipe exp2 (0)
 //  DMHA_ISSUERS = MMA-issuing threads: 1 = one for both Q tiles (D = 128
-//                 default), 2 = one per Q tile, 3 = split S / PV issuers
-//                 (D = 64 only; D = 64 default), 4 = S issuer + one PV issuer
-//                 per Q tile (D = 64 only)
-//  DMHA_SPLIT   = 1: split-row softmax (16 softmax warps)
+//                 default), 2 = one per Q tile (D = 64 split-softmax
+//                 default), 3 = split S / PV issuers (D = 64 only; default of
+//                 the two-warpgroup D = 64 kernel), 4 = S issuer + one PV
+//                 issuer per Q tile (D = 64 only)
+//  DMHA_SPLIT   = 1: split-row softmax (16 softmax warps; D = 64 default)
+struct PingpongConfig {
+  bool split;
+  int iss;
+};
+PingpongConfig pingpong_config(int D) {
+  // D = 64 default: the split softmax (16 softmax warps, two per row) with one
+  // MMA issuer per Q tile (DESIGN.md §5 lessons 16-17)
+  PingpongConfig c{D == 64, 1};
+  if (const char* e = std::getenv("DMHA_SPLIT")) c.split = std::atoi(e) != 0;
+  c.iss = D == 64 ? (c.split ? 2 : 3) : 1;
+  if (const char* e = std::getenv("DMHA_ISSUERS")) c.iss = std::atoi(e);
+  return c;
+}
+
 template <int D>
 cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   int emu = 0;
   if (const char* e = std::getenv("DMHA_EMU")) emu = std::atoi(e);
-  int iss = D == 64 ? 3 : 1;
-  if (const char* e = std::getenv("DMHA_ISSUERS")) iss = std::atoi(e);
-  // D = 64 default: the split softmax (16 softmax warps, two per row) with
-  // split QK^T / PV issuers (DESIGN.md §5 lesson 16); DMHA_SPLIT=0|1 overrides.
-  bool split = (D == 64);
-  if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
+  const PingpongConfig cfg = pingpong_config(D);
+  const int iss = cfg.iss;
+  const bool split = cfg.split;
   if (split) {
+    if (D == 64 && iss == 2) return launch_de<D, 0, true, 2>(a, stream);
     if (D == 64 && iss == 3) {
       switch (emu) {
         case 1: return launch_de<D, 1, true, 3>(a, stream);
@@ -900,17 +913,12 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
-// The fused combine lives in the one-thread-per-row epilogue; the split
-// softmax (two threads per row, DMHA_SPLIT=1) keeps the separate combine.
 bool pingpong_fused_combine_ok(int D) {
   // The one-thread-per-row epilogue merges; so does the split softmax's when
-  // it runs with split issuers (the D = 64 default).  Other split
-  // configurations keep the separate combine pass.
-  bool split = (D == 64);
-  if (const char* e = std::getenv("DMHA_SPLIT")) split = std::atoi(e) != 0;
-  int iss = D == 64 ? 3 : 1;
-  if (const char* e = std::getenv("DMHA_ISSUERS")) iss = std::atoi(e);
-  return !split || (D == 64 && iss == 3);
+  // it runs with per-tile or split issuers (the D = 64 configurations).  The
+  // D = 128 split softmax (single issuer) keeps the separate combine pass.
+  const PingpongConfig c = pingpong_config(D);
+  return !c.split || (D == 64 && (c.iss == 2 || c.iss == 3));
 }
 
 cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t stream) {
