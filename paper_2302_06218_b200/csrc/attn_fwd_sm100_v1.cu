@@ -882,7 +882,7 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   const int iss = cfg.iss;
   const bool split = cfg.split;
   if (split) {
-    if (D == 64 && iss == 2) return launch_de<D, 0, true, 2>(a, stream);
+    if (iss == 2) return launch_de<D, 0, true, 2>(a, stream);
     if (D == 64 && iss == 4) return launch_de<D, 0, true, 4>(a, stream);
     if (D == 64 && iss == 3) {
       switch (emu) {
