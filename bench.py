@@ -4,6 +4,9 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...       (N > 1)
 
+With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py re-launches
+itself under torch.distributed.run with N ranks on 127.0.0.1 (one per GPU).
+
 A step is one full dmha_forward (every hot-path row of SURVEY §8(a): shard
 map, ring K/V exchange, tcgen05 attention, LSE combine) over one batch of
 synthetic input.  Default workload C4 (BASELINE.json configs[3]): L=262144,
@@ -123,12 +126,43 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def spawn_ranks_if_needed(args) -> int | None:
+    """--gpus N > 1 without a torchrun environment: re-launch this script under
+    torch.distributed.run (N ranks, 127.0.0.1, a free port) and return its
+    exit code; None when already inside a launched rank (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 # ----------------------------------------------------------------- CPU oracle baseline
 def cpu_oracle_sample(w, target_s: float = 12.0, seed: int = 4321):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
     `n` query rows of one head against all L keys (same L, D; the per-row cost
     is what the full job would pay L*H times).  Returns (TFLOP/s, cores, desc)."""
     import numpy as np
+    # all of this process's host cores for the OpenMP oracle (torchrun sets
+    # OMP_NUM_THREADS=1 for its ranks; libgomp reads it when the oracle loads)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     from oracle import oracle
     from synth import inputs
     L, D = w["L"], w["D"]
@@ -155,7 +189,7 @@ def cpu_oracle_sample(w, target_s: float = 12.0, seed: int = 4321):
     n = min(n, 1 << 22)
     rate, dt = run(n)
     desc = (f"{n} query rows x 1 head against all L={L} keys (D={D}, causal={w['causal']}), "
-            f"fp64 C/OpenMP oracle, {dt:.1f} s")
+            f"fp64 C/OpenMP oracle, {dt:.1f} s, CPU: {cpu_model()}")
     return rate / 1e12, oracle.num_threads(), desc, dt
 
 
@@ -164,6 +198,7 @@ def run_reference(args, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     from oracle import oracle
     oracle.build()
     times, rates, desc, cores = [], [], "", 1
@@ -181,7 +216,7 @@ def run_reference(args, w):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_of(args, w),
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
-                         "sample": desc},
+                         "sample": desc, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -200,6 +235,80 @@ def config_of(args, w):
 
 
 # ----------------------------------------------------------------- our arm
+NVLINK_DATASHEET_GBS = 900.0  # NVLink 5, per direction per GPU (B200 datasheet)
+
+
+def measure_nccl_sendrecv(dist, dev, world, rank, nbytes=256 << 20, iters=5):
+    """Measured ring send/recv ceiling on this box (torch.distributed NCCL,
+    CUDA-event timed, max over ranks): bytes sent per rank per second."""
+    import torch
+    send = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    recv = torch.empty_like(send)
+
+    def once():
+        ops = [dist.P2POp(dist.isend, send, (rank + 1) % world),
+               dist.P2POp(dist.irecv, recv, (rank - 1) % world)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    once()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        once()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / iters
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return nbytes / (float(t.item()) / 1e3) / 1e9
+
+
+def roofline_of(w, st, steps, world, step_ms_local, peaks, peak_src):
+    """Roofline of the dominant kernel (attention): algorithmic FLOP per
+    launch / its CUDA-event launch time (library events on its own stream)."""
+    L, D = w["L"], w["D"]
+    total_flops = flops(w)
+    attn_ms_avg = st["attn_ms"] / max(1, st["attn_launches"])
+    launches_per_step = st["attn_launches"] / steps
+    flops_per_launch = total_flops / world / max(1.0, launches_per_step)
+    achieved = flops_per_launch / (attn_ms_avg / 1e3) / 1e12
+    attn_share = st["attn_ms"] / steps / step_ms_local if step_ms_local > 0 else None
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(w["name"])
+        except Exception:
+            traffic = None
+    if w["dtype"] == "fp32":
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        return {"bound": "alu", "kernel": "attn_fwd_fp32", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_kind": f"FP32 FMA pipe, 148x128x2 FLOP/clk at {sm_mhz:.0f} MHz (derived)",
+                "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
+                "share_of_step": attn_share}
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    r = {"bound": "tensor", "kernel": f"attn_fwd_sm100_kernel<{D}>", "achieved": achieved,
+         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+         "peak_kind": f"bf16 dense sustained, {peak_src}",
+         "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
+         "frac_of_datasheet_2250": achieved / 2250.0,
+         "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
+         "share_of_step": attn_share}
+    if D == 64:
+        # At D = 64 one exponential (MUFU, 16/clk/SM) per score binds before
+        # the tensor pipe: ceiling = 148 SMs x 16 x 4*D FLOP per clock
+        # (DESIGN.md §5 a2) at the maximum SM clock.
+        mx = float(peaks.get("sm_max_mhz", 1965.0))
+        cap = 148 * 16 * 4 * D * mx * 1e6 / 1e12
+        r["exp_ceiling"] = {"peak_at_max_clock": cap, "frac_at_max_clock": achieved / cap,
+                            "unit": "TFLOP/s",
+                            "pipe": "MUFU ex2, 16/clk/SM (measured, tools/mufu_rate.cu)"}
+    return r
+
+
 def run_ours(args, w):
     import torch
     import torch.distributed as dist
@@ -208,33 +317,20 @@ def run_ours(args, w):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.launch_check:  # CPU test hook: which ranks did the launcher start?
+        print(json.dumps({"rank": rank, "world": world, "gpus": args.gpus}), flush=True)
+        return 0
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    L, D, H = w["L"], w["D"], w["H"]
-    if L % (2 * world if w["layout"] == "zigzag" else world):
-        raise SystemExit("L not divisible for this world size")
-    Lloc = L // world
-    tdt = torch.bfloat16 if w["dtype"] == "bf16" else torch.float32
     stream = torch.cuda.current_stream()
     if world > 1:
         dmha.init_distributed(w["dtype"], w["layout"], local)
     else:
         dmha.init(1, 0, None, local, w["dtype"], w["layout"], stream.cuda_stream)
-
-    gen = torch.Generator(device=dev)
-    shards = []
-    for tid in range(3):  # synthetic N(0,1) shards, seeded per (rank, tensor)
-        gen.manual_seed(1234 * 1000003 + rank * 101 + tid)
-        shards.append(torch.randn((Lloc, H, D), generator=gen, device=dev, dtype=torch.float32).to(tdt))
-    q, k, v = shards
-    out = torch.empty_like(q)
-    lse = torch.empty((H, Lloc), dtype=torch.float32, device=dev)
-    need_flush = Lloc * H * D * q.element_size() <= 126e6
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if need_flush else None
 
     def barrier():
         if world > 1:
@@ -247,92 +343,89 @@ def run_ours(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    fwd = dmha.forward if args.exchange == "ring" else dmha.forward_headpar
-    for _ in range(args.warmup):
-        fwd(q, k, v, L, w["causal"], out, lse)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
+    def make_inputs(wl):
+        L, D, H = wl["L"], wl["D"], wl["H"]
+        if L % (2 * world if wl["layout"] == "zigzag" else world):
+            raise SystemExit("L not divisible for this world size")
+        Lloc = L // world
+        tdt = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float32
+        gen = torch.Generator(device=dev)
+        shards = []
+        for tid in range(3):  # synthetic N(0,1) shards, seeded per (rank, tensor)
+            gen.manual_seed(1234 * 1000003 + rank * 101 + tid)
+            shards.append(torch.randn((Lloc, H, D), generator=gen, device=dev,
+                                      dtype=torch.float32).to(tdt))
+        out = torch.empty_like(shards[0])
+        lse = torch.empty((H, Lloc), dtype=torch.float32, device=dev)
+        return (*shards, out, lse)
 
-    # ---- device-timed region: exactly K steps
-    st0 = dmha.get_stats()
-    dmha.set_profiling(True)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            if flush is not None:
-                flush.fill_(i & 0xFF)
-            evs[i][0].record(stream)
-            fwd(q, k, v, L, w["causal"], out, lse)
-            evs[i][1].record(stream)
+    fwd = dmha.forward if args.exchange == "ring" else dmha.forward_headpar
+
+    def timed_run(wl, steps, warmup):
+        """W untimed warmups, then exactly K device-timed steps (CUDA events on
+        the launch stream, barrier + synchronize on both sides, max over
+        ranks); returns (step_ms, local step_ms, stats delta, clocks, inputs)."""
+        q, k, v, out, lse = make_inputs(wl)
+        Lloc = q.shape[0]
+        need_flush = Lloc * wl["H"] * wl["D"] * q.element_size() <= 126e6
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if need_flush else None
+        for _ in range(warmup):
+            fwd(q, k, v, wl["L"], wl["causal"], out, lse)
         torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    st1 = dmha.get_stats()
-    dmha.set_profiling(False)
-    step_ms_local = sum(a.elapsed_time(b) for a, b in evs) / args.steps
-    step_ms = max_over_ranks(step_ms_local)
+        barrier()
+        torch.cuda.synchronize()
+        st0 = dmha.get_stats()
+        dmha.set_profiling(True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        with ClockSampler(local) as clk:
+            for i in range(steps):
+                if flush is not None:
+                    flush.fill_(i & 0xFF)
+                evs[i][0].record(stream)
+                fwd(q, k, v, wl["L"], wl["causal"], out, lse)
+                evs[i][1].record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        st1 = dmha.get_stats()
+        dmha.set_profiling(False)
+        delta = {key: st1[key] - st0[key] for key in ("kernel_launches", "bytes_sent")}
+        for key in ("attn_ms", "attn_launches", "combine_ms", "combine_launches", "exchange_ms",
+                    "exchanges", "last_bytes_sent", "last_exchanges"):
+            delta[key] = st1[key]  # profiling counters were reset by set_profiling(True)
+        local_ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+        return max_over_ranks(local_ms), local_ms, delta, clk.summary(), (q, k, v, out, lse)
+
+    w = dict(w, name=args.workload)
+    xpeak = measure_nccl_sendrecv(dist, dev, world, rank) if world > 1 else None
+    step_ms, step_ms_local, st, clocks, (q, k, v, out, lse) = timed_run(w, args.steps, args.warmup)
+    L, D, H = w["L"], w["D"], w["H"]
+    Lloc = L // world
     total_flops = flops(w)
     value = total_flops / (step_ms / 1e3) / 1e12
-    launches = st1["kernel_launches"] - st0["kernel_launches"]
-
-    # ---- roofline of the dominant kernel (attention), event-timed per launch
     peaks, peak_src = load_peaks()
-    attn_ms_avg = st1["attn_ms"] / max(1, st1["attn_launches"])
-    launches_per_step = st1["attn_launches"] / args.steps
-    flops_per_launch = total_flops / world / max(1.0, launches_per_step)
-    achieved = flops_per_launch / (attn_ms_avg / 1e3) / 1e12
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        try:
-            traffic = json.loads(tf.read_text()).get(args.workload)
-        except Exception:
-            traffic = None
-    attn_share = st1["attn_ms"] / args.steps / step_ms_local if step_ms_local > 0 else None
-    if w["dtype"] == "fp32":
-        # SIMT fp32 kernel: bound by the FP32 FMA pipe, 148 SMs x 128 lanes x
-        # 2 FLOP per clock at the maximum SM clock (DESIGN.md §5 fp32 path)
-        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-        roofline = {"bound": "alu", "kernel": f"attn_fwd_fp32_kernel<{D}>", "achieved": achieved,
-                    "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                    "peak_kind": f"FP32 FMA pipe, 148x128x2 FLOP/clk at {sm_mhz:.0f} MHz (derived)",
-                    "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
-                    "share_of_step": attn_share}
-    else:
-        roofline = {"bound": "tensor", "kernel": f"attn_fwd_sm100_kernel<{D}>", "achieved": achieved,
-                    "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                    "peak_kind": f"bf16 dense sustained, {peak_src}",
-                    "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
-                    "frac_of_datasheet_2250": achieved / 2250.0,
-                    "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
-                    "share_of_step": attn_share}
-        if D == 64:
-            # At D = 64 one exponential (MUFU, 16/clk/SM) per score binds before
-            # the tensor pipe: ceiling = 148 SMs x 16 x 4*D FLOP per clock
-            # (DESIGN.md §5 a2), at the maximum and at the measured SM clock.
-            mx = float(peaks.get("sm_max_mhz", 1965.0))
-            roofline["exp_ceiling"] = {
-                "peak_at_max_clock": 148 * 16 * 4 * D * mx * 1e6 / 1e12,
-                "frac_at_max_clock": achieved / (148 * 16 * 4 * D * mx * 1e6 / 1e12),
-                "unit": "TFLOP/s", "pipe": "MUFU ex2, 16/clk/SM (measured, tools/mufu_rate.cu)"}
+    roofline = roofline_of(w, st, args.steps, world, step_ms_local, peaks, peak_src)
+    peak = roofline["peak"]
     secondary = {}
-    if st1["combine_launches"]:
-        cm = st1["combine_ms"] / st1["combine_launches"]
+    if st["combine_launches"]:
+        cm = st["combine_ms"] / st["combine_launches"]
         cbytes = 12.0 * Lloc * H * D + 12.0 * Lloc * H
         secondary["combine"] = {"bound": "hbm", "achieved": cbytes / (cm / 1e3) / 1e9,
                                 "peak": float(peaks.get("hbm_gbs", 6551.7)), "unit": "GB/s",
                                 "launch_ms": cm}
         secondary["combine"]["frac"] = secondary["combine"]["achieved"] / secondary["combine"]["peak"]
-    if st1["exchanges"]:
-        xm = st1["exchange_ms"] / st1["exchanges"]
+    if st["exchanges"]:
+        xm = st["exchange_ms"] / st["exchanges"]
         xbytes = 2.0 * Lloc * H * D * q.element_size()
-        secondary["exchange"] = {"bound": "nvlink", "achieved": xbytes / (xm / 1e3) / 1e9,
-                                 "peak": 770.0, "unit": "GB/s", "launch_ms": xm,
-                                 "note": "per-direction bytes sent per ring step / event time on the comm stream"}
+        ach = xbytes / (xm / 1e3) / 1e9
+        secondary["exchange"] = {
+            "bound": "nvlink", "achieved": ach, "unit": "GB/s", "launch_ms": xm,
+            "peak": NVLINK_DATASHEET_GBS, "frac": ach / NVLINK_DATASHEET_GBS,
+            "peak_kind": "NVLink 5 datasheet, 900 GB/s per direction per GPU",
+            "peak_measured_nccl_sendrecv": xpeak,
+            "frac_of_measured": (ach / xpeak) if xpeak else None,
+            "note": "bytes sent per ring step / CUDA-event time of the exchange on the comm stream"}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -352,12 +445,27 @@ def run_ours(args, w):
                "h2d_bytes_per_step": 3 * hq.numel() * hq.element_size(),
                "d2h_bytes_per_step": hout.numel() * hout.element_size() + hlse.numel() * 4,
                "ms_per_step": 1e3 * t_e2e}
+        del hq, hk, hv, hout, hlse
+    del q, k, v, out, lse
 
-    # ---- CPU oracle baseline (rank 0, N == 1 only)
+    # ---- the north-star head shape (C5, D = 64 causal) device-timed at N = 1
+    if world == 1 and args.workload != "C5" and w["dtype"] == "bf16" and not args.no_secondary:
+        w5 = dict(WORKLOADS["C5"], name="C5")
+        torch.cuda.empty_cache()
+        ms5, ms5_local, st5, clk5, _ = timed_run(w5, 3, 1)
+        torch.cuda.empty_cache()
+        secondary["C5"] = {"workload": w5["desc"], "value": flops(w5) / (ms5 / 1e3) / 1e12,
+                           "unit": "TFLOP/s", "ms_per_step": ms5, "steps": 3, "warmup": 1,
+                           "roofline": roofline_of(w5, st5, 3, 1, ms5_local, peaks, peak_src),
+                           "clocks": clk5}
+
+    # ---- CPU oracle baseline (rank 0, every N; the other ranks wait at a barrier)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         rate, cores, desc, _ = cpu_oracle_sample(w)
-        cpu = {"value": rate, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = {"value": rate, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "cpu_model": cpu_model()}
+    barrier()
 
     if rank == 0:
         line = {
@@ -365,12 +473,13 @@ def run_ours(args, w):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": w["dtype"], "data": "synthetic", "config": config_of(args, w),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(st["kernel_launches"]), "clocks": clocks,
             "pct_of_peak": {"measured_sustained": value / (peak * world),
                             "datasheet_2250": value / (2250.0 * world)},
             "secondary": secondary or None,
-            "bytes_sent_per_step": (st1["bytes_sent"] - st0["bytes_sent"]) / args.steps,
+            "bytes_sent_per_step": st["bytes_sent"] / args.steps,
+            "bytes_sent_last_forward": st["last_bytes_sent"],
         }
         print(json.dumps(line), flush=True)
     dmha.finalize()
@@ -390,7 +499,13 @@ def main():
                     help="ring (north_star, default) or the paper's all-to-all head-parallel exchange")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary C5 line (N=1)")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="(test hook) each launched rank prints its rank/world and exits")
     args = ap.parse_args()
+    rc = spawn_ranks_if_needed(args)
+    if rc is not None:
+        return rc
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("BENCH_ALLOW_SHORT_WARMUP"):
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     w = WORKLOADS[args.workload]

@@ -76,9 +76,17 @@ struct dmha_stats {
   double attn_ms;            /* summed attention kernel time                      */
   double combine_ms;         /* summed combine kernel time                        */
   double exchange_ms;        /* summed send/recv time on the comm stream          */
+  /* Per-forward accounting, reset at the start of every forward call and
+   * counted at each send: bytes this rank sent (the emulated entry points sum
+   * their P ranks) and the number of exchanges (ring steps / all-to-all
+   * blocks).  Ring: exactly (P-1) * 2 * L_loc*H*D*elem per rank. */
+  uint64_t last_bytes_sent;
+  uint64_t last_exchanges;
 };
 
-/* ---- setup / teardown ---------------------------------------------------- */
+/* ---- setup / teardown ----------------------------------------------------
+ * SURVEY.md §8(b) (the C-ABI boundary) and §3c: one process per GPU; the NCCL
+ * communicator realises the "N GPUs in one node" of PAPER.md:664-668. */
 
 /* Rank 0 only, before dmha_init with world_size > 1: writes a 128-byte NCCL
  * unique id to id_out; the caller broadcasts it (e.g. torch.distributed). */
@@ -111,6 +119,14 @@ const char *dmha_last_error(void);
  * accumulator (north_star (3)) — for bf16 fused into the attention kernel's
  * epilogue (env DMHA_FUSED_COMBINE=0 selects the
  * separate combine kernel, bit-identical result).
+ * Ordering: the exchange of step s runs on a library comm stream and lands
+ * in ring buffer (s+1)%2 after the attention of step s-1 (that buffer's last
+ * reader) finished; the attention of step s+1 waits for it.  One NVTX range
+ * per ring step ("dmha ring rank r step s src j") brackets the enqueue.
+ * Debug: DMHA_CHECK_COLLECTIVE=1 cross-checks (L, D, H, causal) over the
+ * ranks with two tiny all-reduces first (INVALID on a mismatch);
+ * DMHA_FAULT=perturb_lse adds 0.5 to every partial lse inside the combine
+ * (fault injection: the parity suite must then fail).
  * Errors: INVALID (null, sizes, misaligned, out/lse overlapping q/k/v),
  * UNSUPPORTED (D), STATE, OOM, CUDA, NCCL. */
 int dmha_forward(const void *q, const void *k, const void *v, void *out, float *lse,
@@ -129,11 +145,14 @@ int dmha_forward_host(const void *q, const void *k, const void *v, void *out, fl
 
 /* Single-GPU emulation of the P-rank ring (test/measurement hook): q/k/v/out
  * are DEVICE [P][L_loc, H, D] buffers holding every rank's shard back to back
- * (rank-major), lse is [P][H, L_loc].  Runs each rank's ring schedule in turn
- * with the identical kernels, index math and combine order as dmha_forward at
- * world_size P, moving K/V blocks with device copies instead of NCCL.  No two
- * kernels wait on one another.  Uses the dtype/stream of dmha_init (which may
- * have world_size 1). */
+ * (rank-major), lse is [P][H, L_loc].  Runs each rank's ring in turn through
+ * the SAME loop as dmha_forward at world_size P — the two K/V ring buffers,
+ * the comm stream, the recv/compute events and the buffer-reuse rule — with a
+ * single-GPU transport: each receive is one cudaMemcpyAsync per K and per V
+ * block on the comm stream from the sending rank's shard (what NCCL would
+ * deliver), overlapping the attention on the compute stream.  No two kernels
+ * wait on one another.  Uses the dtype/stream of dmha_init (which may have
+ * world_size 1).  Overlap checks cover all P shards. */
 int dmha_forward_emulated(int world_size, int layout, const void *q, const void *k,
                           const void *v, void *out, float *lse, int64_t L, int D, int H,
                           int causal);
@@ -169,17 +188,28 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void *q, con
                                   const void *v, void *out, float *lse, int64_t L, int D, int H,
                                   int causal);
 
-/* Device bytes the ring will hold per rank for (L, D, H) at the initialised
- * world size and dtype: 2 K/V receive buffers (2 * 2 * L_loc*H*D*elem) + the
+/* Library workspace (SURVEY §8(d) max-L footprint): device bytes a forward
+ * of (L, D, H) allocates per rank at the initialised world size and dtype.
+ * World size P > 1: 2 K/V receive buffers (2 * 2 * L_loc*H*D*elem) + the
  * fp32 accumulator O_acc and lse_acc (+ the O_part / lse_part partial buffers
- * when the combine is not fused).  0 at world size 1.  Staging buffers of
- * dmha_forward_host are not included. */
+ * when the combine is not fused).  World size 1: 0, except on small grids
+ * (< 4 waves of 256-row CTAs, L >= 2048, bf16) where the split-KV launch
+ * holds two fp32 partials: 2 * (L*H*D*4 + L*H*4).  Staging buffers of
+ * dmha_forward_host are not included.  A fresh library that runs one forward
+ * holds exactly this (dmha_stats.workspace_bytes).  Errors: STATE, INVALID,
+ * UNSUPPORTED (D). */
 int dmha_workspace_bytes(int64_t L, int D, int H, size_t *bytes_out);
 
-/* Synchronises outstanding profiled work, then copies the counters. */
+/* Same for an explicit world size (what dmha_forward_emulated at world_size
+ * holds, which runs each rank with one set of ring buffers). */
+int dmha_ring_workspace_bytes(int world_size, int64_t L, int D, int H, size_t *bytes_out);
+
+/* SURVEY §8(c) "Accounting" and §8(d): synchronises outstanding profiled
+ * work, then copies the counters into *s (caller-owned).  INVALID if null. */
 int dmha_get_stats(struct dmha_stats *s);
 
-/* enable != 0: bracket every library kernel launch and ring exchange with CUDA
+/* SURVEY §8(d) measurement hook.
+ * enable != 0: bracket every library kernel launch and ring exchange with CUDA
  * events on its own stream and accumulate their durations into dmha_stats
  * (measurement hook used by bench.py); enable == 0 stops it.  Also resets the
  * timed counters. */

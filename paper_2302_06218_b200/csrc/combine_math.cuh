@@ -1,7 +1,7 @@
 // combine_math.cuh — the log-sum-exp merge of one ring-step partial into the
 // running accumulator (north_star (3)), shared by the
 // stand-alone combine kernel (lse_combine.cu) and the attention epilogue's
-// fused combine (attn_fwd_sm100_v1.cu, NEXT-2), so both produce the same bits:
+// fused combine (attn_fwd_sm100.cu, NEXT-2), so both produce the same bits:
 //   lse = M + ln(e^{lse_a - M} + e^{lse_s - M}),   M = max(lse_a, lse_s)
 //   O   = O_a e^{lse_a - lse} + O_s e^{lse_s - lse}
 // A -inf lse (no usable key) weighs 0; two -inf stay -inf with O = 0

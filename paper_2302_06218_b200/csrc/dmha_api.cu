@@ -18,6 +18,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -93,6 +94,10 @@ struct State {
   float* st_lse = nullptr;
   size_t st_bytes = 0, st_lse_elems = 0;
   dmha_stats stats{};
+  // Fault injection (DMHA_FAULT=perturb_lse, read at every forward): the
+  // log-sum-exp combine adds this to each partial's lse, so the merged
+  // output is wrong whenever a combine runs (test that the suite notices).
+  float fault_lse_bias = 0.f;
   // profiling (dmha_set_profiling)
   bool profile = false;
   struct Rec {
@@ -192,6 +197,28 @@ bool fused_combine(int D) {
   return g.dtype == DMHA_BF16 && dmha::attn_fused_combine_supported(D);
 }
 
+// Split-KV for a P = 1 forward on a small grid (fewer than 4 waves of
+// 256-row CTAs, Lloc >= 2048; DMHA_KV_SPLIT=0 disables): two fp32 partials
+// merged by the log-sum-exp combine (DESIGN.md §5 lesson 14).
+bool split_kv_active(int64_t Lloc, int D, int H) {
+  const int64_t ctas = (Lloc + 255) / 256 * H;
+  const char* e = std::getenv("DMHA_KV_SPLIT");
+  return g.dtype == DMHA_BF16 && ctas < 4 * 148 && Lloc >= 2048 && !(e && std::atoi(e) == 0) &&
+         dmha::attn_kv_split_supported(D);
+}
+
+// Device bytes a forward at world size P holds (the buffers ensure_ring_ws
+// allocates for it): P = 1 only the split-KV partials (O_acc, O_part,
+// lse_acc, lse_part) when split_kv_active; P > 1 two K/V ring buffers, O_acc
+// and lse_acc, plus O_part / lse_part when the combine is not fused.
+size_t ring_ws_bytes(int P, int64_t Lloc, int D, int H) {
+  const size_t elems = static_cast<size_t>(Lloc) * H * D;
+  const size_t lse = static_cast<size_t>(Lloc) * H;
+  if (P == 1) return split_kv_active(Lloc, D, H) ? 2 * (elems * 4 + lse * 4) : 0;
+  const size_t parts = fused_combine(D) ? 1 : 2;
+  return 2 * (2 * elems * elem_bytes(g.dtype)) + parts * (elems * 4 + lse * 4);
+}
+
 // Ring accumulators (always), the partial buffers (unfused combine only) and
 // the K/V ring buffers (need_kv).
 int ensure_ring_ws(int64_t Lloc, int D, int H, bool need_kv, bool force_part = false) {
@@ -277,8 +304,10 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   return pa < pb + nb && pb < pa + na;
 }
 
+// nshards: how many [L_loc, H, D] shards each buffer holds back to back (the
+// emulated entry points pass P rank-major shards), for the overlap check.
 int validate(const void* q, const void* k, const void* v, const void* out, const float* lse,
-             int64_t L, int D, int H, int P, int layout) {
+             int64_t L, int D, int H, int P, int layout, int nshards = 1) {
   if (!q || !k || !v || !out || !lse) return fail(DMHA_ERR_INVALID, "dmha: null pointer");
   if (L < 1 || H < 1) return fail(DMHA_ERR_INVALID, "dmha: need L >= 1 and H >= 1");
   if (D != 64 && D != 128)
@@ -295,8 +324,8 @@ int validate(const void* q, const void* k, const void* v, const void* out, const
   for (const void* p : ptrs)
     if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
       return fail(DMHA_ERR_INVALID, "dmha: base pointers must be 16-byte aligned");
-  const size_t tb = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
-  const size_t lb = static_cast<size_t>(Lloc) * H * 4;
+  const size_t tb = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype) * nshards;
+  const size_t lb = static_cast<size_t>(Lloc) * H * 4 * nshards;
   const void* ins[3] = {q, k, v};
   for (const void* in : ins)
     if (overlaps(out, tb, in, tb) || overlaps(lse, lb, in, tb))
@@ -315,6 +344,7 @@ int run_local(const void* q, const void* k, const void* v, void* out, float* lse
   a.kv_split = kv_split;
   a.out2 = out2;
   a.lse2 = lse2;
+  a.lse_bias = g.fault_lse_bias;
   a.q = q;
   a.k = k;
   a.v = v;
@@ -345,7 +375,7 @@ int run_combine(float* o_part, float* lse_part, void* out, float* lse, int64_t L
   cudaError_t e = cudaSuccess;
   timed(1, g.stream, [&]() {
     e = dmha::launch_lse_combine(g.o_acc, g.lse_acc, o_part, lse_part, out, lse, Lq, D, H,
-                                 final_step, g.dtype == DMHA_BF16, g.stream);
+                                 final_step, g.dtype == DMHA_BF16, g.stream, g.fault_lse_bias);
     return 0;
   });
   if (e != cudaSuccess)
@@ -389,11 +419,7 @@ int ring_compute_step(int s, int P, int r, int layout, const void* q, const void
       // Small grids (fewer than 4 waves of 256-row CTAs, e.g. C2) leave SMs
       // idle in the last wave: split each row block's keys over two CTAs
       // and merge the two fp32 partials with the log-sum-exp combine.
-      const int64_t ctas = (Lloc + 255) / 256 * H;
-      const char* e = std::getenv("DMHA_KV_SPLIT");
-      const bool split = g.dtype == DMHA_BF16 && ctas < 4 * 148 && Lloc >= 2048 &&
-                         !(e && std::atoi(e) == 0) && dmha::attn_kv_split_supported(D);
-      if (!split)
+      if (!split_kv_active(Lloc, D, H))
         return run_local(q, ks, vs, out, lse, Lloc, Lloc, D, H, causal, qm, km, dmha::OUT_FINAL);
       if (int rc = ensure_ring_ws(Lloc, D, H, false, true)) return rc;
       if (int rc = run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
@@ -430,6 +456,143 @@ int poll_nccl() {
     return fail(DMHA_ERR_NCCL, "dmha: NCCL async error: %s",
                 ncclGetErrorString(r != ncclSuccess ? r : st));
   }
+  return DMHA_OK;
+}
+
+// ---------------------------------------------------------------- a3 ring
+// The K/V exchange of one ring step: at step s rank r sends
+// the block it attends (kcur, vcur) to r+1 and receives the block of step
+// s+1 from r-1 into ring buffer `dst` (K then V, blk bytes each), enqueued
+// on the comm stream.  Two implementations share the loop below:
+//   NcclTransport  grouped ncclSend / ncclRecv over NVLink (dmha_forward);
+//   CopyTransport  the single-GPU emulation (dmha_forward_emulated): one
+//                  cudaMemcpyAsync per K / V block from the shard rank r-1
+//                  holds at step s (rank (r-1-s) mod P's original block).
+struct Transport {
+  virtual ~Transport() = default;
+  virtual int exchange(const dmha_ring_plan& pl, int s, const void* kcur, const void* vcur,
+                       char* dst, size_t blk) = 0;
+};
+
+struct NcclTransport final : Transport {
+  int exchange(const dmha_ring_plan& pl, int, const void* kcur, const void* vcur, char* dst,
+               size_t blk) override {
+    CK_NCCL(ncclGroupStart());
+    CK_NCCL(ncclSend(kcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
+    CK_NCCL(ncclSend(vcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
+    CK_NCCL(ncclRecv(dst, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
+    CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
+    CK_NCCL(ncclGroupEnd());
+    return DMHA_OK;
+  }
+};
+
+struct CopyTransport final : Transport {
+  const char *k_all, *v_all;  // [P][L_loc, H, D] shards, rank-major
+  size_t shard;
+  int P, r, layout;
+  int64_t L;
+  CopyTransport(const char* k, const char* v, size_t sh, int P_, int r_, int lay, int64_t L_)
+      : k_all(k), v_all(v), shard(sh), P(P_), r(r_), layout(lay), L(L_) {}
+  int exchange(const dmha_ring_plan& pl, int s, const void*, const void*, char* dst,
+               size_t blk) override {
+    // what rank recv_from sends at step s is the block it attends at step s,
+    // i.e. rank (recv_from - s) mod P's shard == the src of our step s+1
+    const int src_next = make_plan(P, r, s + 1, layout, L).src;
+    if (src_next != ((pl.recv_from - s) % P + P) % P)
+      return fail(DMHA_ERR_STATE, "dmha: ring plan inconsistent at rank %d step %d", r, s);
+    CK_CUDA(cudaMemcpyAsync(dst, k_all + src_next * shard, blk, cudaMemcpyDeviceToDevice, g.comm));
+    CK_CUDA(cudaMemcpyAsync(dst + blk, v_all + src_next * shard, blk, cudaMemcpyDeviceToDevice,
+                            g.comm));
+    return DMHA_OK;
+  }
+};
+
+// Per-forward accounting (dmha_stats.last_*): reset at every public forward,
+// counted at each send (one exchange = one call).
+void begin_forward() {
+  g.stats.last_bytes_sent = 0;
+  g.stats.last_exchanges = 0;
+  const char* f = std::getenv("DMHA_FAULT");
+  g.fault_lse_bias = (f && !strcmp(f, "perturb_lse")) ? 0.5f : 0.f;
+}
+void count_sent(uint64_t bytes) {
+  g.stats.bytes_sent += bytes;
+  g.stats.last_bytes_sent += bytes;
+  g.stats.last_exchanges++;
+}
+
+// One rank's distributed forward: P-1 exchange steps on the comm
+// stream, each overlapped with the attention of the current block on the
+// compute stream.  Ordering (per buffer b in {0,1}):
+//   recv into b at step s      waits ev_done[b] of the compute of step s-1
+//                              (the buffer's last reader; plan field
+//                              recv_after_compute_of) — the previous block
+//                              is gone only after its attention finished;
+//   compute of step s+1        waits ev_recv[b] (the block has landed).
+int ring_forward(int P, int r, int layout, const void* q, const void* k, const void* v, void* out,
+                 float* lse, int64_t L, int D, int H, int causal, Transport& tx) {
+  if (P == 1) return ring_compute_step(0, 1, 0, layout, q, k, v, out, lse, L, D, H, causal);
+  const int64_t Lloc = L / P;
+  if (int rc = ensure_ring_ws(Lloc, D, H, true)) return rc;
+  const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+  CK_CUDA(cudaEventRecord(g.ev_start, g.stream));
+  CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_start, 0));
+  const void* kcur = k;
+  const void* vcur = v;
+  char name[64];
+  for (int s = 0; s < P; ++s) {
+    const dmha_ring_plan pl = make_plan(P, r, s, layout, L);
+    snprintf(name, sizeof(name), "dmha ring rank %d step %d src %d", r, s, pl.src);
+    nvtxRangePushA(name);
+    if (pl.recv_buf >= 0) {
+      const int nb = pl.recv_buf;
+      if (pl.recv_after_compute_of >= 0) CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_done[nb], 0));
+      char* dst = static_cast<char*>(g.kvbuf[nb]);
+      int rc = timed(2, g.comm, [&]() { return tx.exchange(pl, s, kcur, vcur, dst, blk); });
+      if (rc) {
+        nvtxRangePop();
+        return rc;
+      }
+      CK_CUDA(cudaEventRecord(g.ev_recv[nb], g.comm));
+      count_sent(2 * blk);
+    }
+    int rc = ring_compute_step(s, P, r, layout, q, kcur, vcur, out, lse, L, D, H, causal);
+    nvtxRangePop();
+    if (rc) return rc;
+    if (pl.compute_buf >= 0) CK_CUDA(cudaEventRecord(g.ev_done[pl.compute_buf], g.stream));
+    g.stats.ring_steps++;
+    if (pl.recv_buf >= 0) {
+      const int nb = pl.recv_buf;
+      CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_recv[nb], 0));
+      kcur = g.kvbuf[nb];
+      vcur = static_cast<char*>(g.kvbuf[nb]) + blk;
+    }
+  }
+  // The comm stream's last work must be ordered before any later reuse.
+  CK_CUDA(cudaEventRecord(g.ev_comm_end, g.comm));
+  CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_comm_end, 0));
+  return DMHA_OK;
+}
+
+// Collective contract (dmha.h): every rank passes the same (L, D, H, causal).
+// With DMHA_CHECK_COLLECTIVE=1 (debug) the values are cross-checked by a min
+// and a max all-reduce before the ring starts (a mismatch would otherwise
+// deadlock or corrupt the exchange).
+int check_collective_contract(int64_t L, int D, int H, int causal) {
+  const char* e = std::getenv("DMHA_CHECK_COLLECTIVE");
+  if (!e || std::atoi(e) == 0 || g.world == 1 || !g.nccl) return DMHA_OK;
+  int64_t h[8] = {L, D, H, causal ? 1 : 0, -L, -D, -H, causal ? -1 : 0};
+  int64_t* d = nullptr;
+  CK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), g.stream));
+  CK_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, g.stream));
+  CK_NCCL(ncclAllReduce(d, d, 8, ncclInt64, ncclMax, g.nccl, g.stream));
+  CK_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, g.stream));
+  CK_CUDA(cudaFreeAsync(d, g.stream));
+  CK_CUDA(cudaStreamSynchronize(g.stream));
+  if (h[0] != L || h[1] != D || h[2] != H || h[3] != (causal ? 1 : 0) || -h[4] != L || -h[5] != D ||
+      -h[6] != H || -h[7] != (causal ? 1 : 0))
+    return fail(DMHA_ERR_INVALID, "dmha: collective contract violated: ranks disagree on (L, D, H, causal)");
   return DMHA_OK;
 }
 
@@ -626,15 +789,15 @@ int dmha_finalize(void) {
 
 int dmha_workspace_bytes(int64_t L, int D, int H, size_t* bytes_out) {
   if (int rc = check_state()) return rc;
-  if (!bytes_out || L < 1 || H < 1 || L % g.world) return fail(DMHA_ERR_INVALID, "dmha_workspace_bytes: bad args");
-  if (g.world == 1) {
-    *bytes_out = 0;
-    return DMHA_OK;
-  }
-  const size_t elems = static_cast<size_t>(L / g.world) * H * D;
-  const size_t lse = static_cast<size_t>(L / g.world) * H;
-  const size_t parts = fused_combine(D) ? 1 : 2;  // O_acc (+ O_part unless fused)
-  *bytes_out = 2 * (2 * elems * elem_bytes(g.dtype)) + parts * (elems * 4 + lse * 4);
+  return dmha_ring_workspace_bytes(g.world, L, D, H, bytes_out);
+}
+
+int dmha_ring_workspace_bytes(int world_size, int64_t L, int D, int H, size_t* bytes_out) {
+  if (int rc = check_state()) return rc;
+  if (!bytes_out || world_size < 1 || L < 1 || H < 1 || L % world_size)
+    return fail(DMHA_ERR_INVALID, "dmha_workspace_bytes: bad args");
+  if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_workspace_bytes: D=%d", D);
+  *bytes_out = ring_ws_bytes(world_size, L / world_size, D, H);
   return DMHA_OK;
 }
 
@@ -684,55 +847,11 @@ int dmha_forward(const void* q, const void* k, const void* v, void* out, float* 
   if (int rc = check_state()) return rc;
   if (int rc = validate(q, k, v, out, lse, L, D, H, g.world, g.layout)) return rc;
   if (int rc = poll_nccl()) return rc;
-  const int P = g.world, r = g.rank;
-  causal = causal ? 1 : 0;
-  if (P == 1) {
-    int rc = ring_compute_step(0, 1, 0, g.layout, q, k, v, out, lse, L, D, H, causal);
-    if (rc) return rc;
-    g.stats.forwards++;
-    return DMHA_OK;
-  }
-  const int64_t Lloc = L / P;
-  if (int rc = ensure_ring_ws(Lloc, D, H, true)) return rc;
-  const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
-  CK_CUDA(cudaEventRecord(g.ev_start, g.stream));
-  CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_start, 0));
-  const void* kcur = k;
-  const void* vcur = v;
-  for (int s = 0; s < P; ++s) {
-    const dmha_ring_plan pl = make_plan(P, r, s, g.layout, L);
-    if (pl.recv_buf >= 0) {
-      const int nb = pl.recv_buf;
-      // the buffer's last reader was the compute of step s-1
-      if (pl.recv_after_compute_of >= 0) CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_done[nb], 0));
-      char* dst = static_cast<char*>(g.kvbuf[nb]);
-      int rc = timed(2, g.comm, [&]() {
-        CK_NCCL(ncclGroupStart());
-        CK_NCCL(ncclSend(kcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
-        CK_NCCL(ncclSend(vcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
-        CK_NCCL(ncclRecv(dst, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
-        CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
-        CK_NCCL(ncclGroupEnd());
-        return static_cast<int>(DMHA_OK);
-      });
-      if (rc) return rc;
-      CK_CUDA(cudaEventRecord(g.ev_recv[nb], g.comm));
-      g.stats.bytes_sent += 2 * blk;
-    }
-    int rc = ring_compute_step(s, P, r, g.layout, q, kcur, vcur, out, lse, L, D, H, causal);
-    if (rc) return rc;
-    if (pl.compute_buf >= 0) CK_CUDA(cudaEventRecord(g.ev_done[pl.compute_buf], g.stream));
-    g.stats.ring_steps++;
-    if (pl.recv_buf >= 0) {
-      const int nb = pl.recv_buf;
-      CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_recv[nb], 0));
-      kcur = g.kvbuf[nb];
-      vcur = static_cast<char*>(g.kvbuf[nb]) + blk;
-    }
-  }
-  // The comm stream's last work must be ordered before any later reuse.
-  CK_CUDA(cudaEventRecord(g.ev_comm_end, g.comm));
-  CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_comm_end, 0));
+  if (int rc = check_collective_contract(L, D, H, causal)) return rc;
+  begin_forward();
+  NcclTransport tx;
+  if (int rc = ring_forward(g.world, g.rank, g.layout, q, k, v, out, lse, L, D, H, causal ? 1 : 0, tx))
+    return rc;
   g.stats.forwards++;
   return DMHA_OK;
 }
@@ -741,6 +860,7 @@ int dmha_forward_host(const void* q, const void* k, const void* v, void* out, fl
                       int64_t L, int D, int H, int causal) {
   if (int rc = check_state()) return rc;
   if (!q || !k || !v || !out || !lse) return fail(DMHA_ERR_INVALID, "dmha_forward_host: null pointer");
+  begin_forward();
   if (L < 1 || H < 1 || L % g.world) return fail(DMHA_ERR_INVALID, "dmha_forward_host: bad L/H");
   const int64_t Lloc = L / g.world;
   const size_t tb = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
@@ -876,28 +996,23 @@ int dmha_forward_emulated(int world_size, int layout, const void* q, const void*
                           void* out, float* lse, int64_t L, int D, int H, int causal) {
   if (int rc = check_state()) return rc;
   if (world_size < 1) return fail(DMHA_ERR_INVALID, "dmha_forward_emulated: world_size < 1");
-  if (int rc = validate(q, k, v, out, lse, L, D, H, world_size, layout)) return rc;
+  if (int rc = validate(q, k, v, out, lse, L, D, H, world_size, layout, world_size)) return rc;
   const int P = world_size;
   const int64_t Lloc = L / P;
-  causal = causal ? 1 : 0;
   const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
-  if (P > 1)
-    if (int rc = ensure_ring_ws(Lloc, D, H, false)) return rc;
-  // Rank r's computation depends only on the inputs, so ranks run one after the
-  // other with a single set of accumulators; the K/V block of step s is read
-  // in place from the source rank's shard (bit-identical to what NCCL delivers).
+  begin_forward();
+  // Rank r's ring runs through the same loop, buffers, events and streams as
+  // dmha_forward at world size P; only the transport differs: each receive is
+  // one cudaMemcpyAsync per K / V block on the comm stream from the sending
+  // rank's shard.  Ranks run one after the other (no kernel waits on another).
   for (int r = 0; r < P; ++r) {
-    const char* qr = static_cast<const char*>(q) + r * blk;
-    char* outr = static_cast<char*>(out) + r * blk;
-    float* lser = lse + static_cast<size_t>(r) * Lloc * H;
-    for (int s = 0; s < P; ++s) {
-      const int src = make_plan(P, r, s, layout, L).src;
-      const char* ks = static_cast<const char*>(k) + src * blk;
-      const char* vs = static_cast<const char*>(v) + src * blk;
-      if (int rc = ring_compute_step(s, P, r, layout, qr, ks, vs, outr, lser, L, D, H, causal)) return rc;
-      if (s < P - 1) g.stats.bytes_sent += 2 * blk;
-      g.stats.ring_steps++;
-    }
+    CopyTransport tx(static_cast<const char*>(k), static_cast<const char*>(v), blk, P, r, layout, L);
+    if (int rc = ring_forward(P, r, layout, static_cast<const char*>(q) + r * blk,
+                              static_cast<const char*>(k) + r * blk,
+                              static_cast<const char*>(v) + r * blk,
+                              static_cast<char*>(out) + r * blk,
+                              lse + static_cast<size_t>(r) * Lloc * H, L, D, H, causal ? 1 : 0, tx))
+      return rc;
   }
   g.stats.forwards++;
   return DMHA_OK;
@@ -912,6 +1027,8 @@ int dmha_forward_headpar(const void* q, const void* k, const void* v, void* out,
   const int P = g.world, r = g.rank;
   causal = causal ? 1 : 0;
   if (P == 1) return dmha_forward(q, k, v, out, lse, L, D, H, causal);
+  if (int rc = check_collective_contract(L, D, H, causal)) return rc;
+  begin_forward();
   const int64_t Lloc = L / P;
   const HpLayout y = hp_layout(P, Lloc, H, D, elem_bytes(g.dtype));
   if (int rc = ensure_hp(y.total)) return rc;
@@ -923,9 +1040,9 @@ int dmha_forward_headpar(const void* q, const void* k, const void* v, void* out,
     for (int d = 0; d < P; ++d) {
       CK_NCCL(ncclSend(ws + send_off + d * blk, blk, ncclChar, d, g.nccl, g.stream));
       CK_NCCL(ncclRecv(ws + recv_off + d * blk, blk, ncclChar, d, g.nccl, g.stream));
+      if (d != r) count_sent(blk);
     }
     CK_NCCL(ncclGroupEnd());
-    g.stats.bytes_sent += (P - 1) * blk;
     return DMHA_OK;
   };
   auto ex1 = [&]() -> int { return a2a(y.send1, y.recv1, y.qkv_blk); };
@@ -937,9 +1054,9 @@ int dmha_forward_headpar(const void* q, const void* k, const void* v, void* out,
       CK_NCCL(ncclSend(ws + y.send_lse + d * y.lse_blk, y.lse_blk, ncclChar, d, g.nccl, g.stream));
       CK_NCCL(ncclRecv(reinterpret_cast<char*>(lse) + d * y.lse_blk, y.lse_blk, ncclChar, d,
                        g.nccl, g.stream));
+      if (d != r) count_sent(y.lse_blk);
     }
     CK_NCCL(ncclGroupEnd());
-    g.stats.bytes_sent += (P - 1) * y.lse_blk;
     return DMHA_OK;
   };
   int rc = headpar_rank(P, r, g.layout, q, k, v, out, lse, L, D, H, causal, ws, y, ex1, ex2, true);
@@ -953,7 +1070,7 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
                                   int causal) {
   if (int rc = check_state()) return rc;
   if (world_size < 1) return fail(DMHA_ERR_INVALID, "dmha_forward_headpar_emulated: world_size < 1");
-  if (int rc = validate(q, k, v, out, lse, L, D, H, world_size, layout)) return rc;
+  if (int rc = validate(q, k, v, out, lse, L, D, H, world_size, layout, world_size)) return rc;
   if (int rc = validate_headpar(world_size, L, H)) return rc;
   const int P = world_size;
   const int64_t Lloc = L / P;
@@ -963,6 +1080,7 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
   const size_t lshard = static_cast<size_t>(Lloc) * H * 4;
   const HpLayout y = hp_layout(P, Lloc, H, D, e);
   if (int rc = ensure_hp(P * y.total)) return rc;
+  begin_forward();
   char* base = static_cast<char*>(g.hp);
   auto ws_of = [&](int r) { return base + static_cast<size_t>(r) * y.total; };
   auto nothing = []() -> int { return DMHA_OK; };
@@ -975,10 +1093,11 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
                                             ws_of(r) + y.send1, geo, static_cast<int>(e), g.stream));
   }
   for (int s = 0; s < P; ++s)
-    for (int d = 0; d < P; ++d)
+    for (int d = 0; d < P; ++d) {
       CK_CUDA(cudaMemcpyAsync(ws_of(d) + y.recv1 + s * y.qkv_blk, ws_of(s) + y.send1 + d * y.qkv_blk,
                               y.qkv_blk, cudaMemcpyDeviceToDevice, g.stream));
-  g.stats.bytes_sent += static_cast<uint64_t>(P) * (P - 1) * y.qkv_blk;
+      if (d != s) count_sent(y.qkv_blk);
+    }
   // Phase 2: per rank unpack, attention for its heads, pack (no-op exchanges).
   for (int r = 0; r < P; ++r) {
     const int64_t Lg = L;
@@ -1005,8 +1124,8 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
       CK_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(lse) + d * lshard + s * y.lse_blk,
                               ws_of(s) + y.send_lse + d * y.lse_blk, y.lse_blk,
                               cudaMemcpyDeviceToDevice, g.stream));
+      if (d != s) count_sent(y.out_blk + y.lse_blk);
     }
-  g.stats.bytes_sent += static_cast<uint64_t>(P) * (P - 1) * (y.out_blk + y.lse_blk);
   for (int r = 0; r < P; ++r) {
     const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
     CK_LAUNCH(dmha::launch_headpar_unpack_out(ws_of(r) + y.recv2, static_cast<char*>(out) + r * shard,

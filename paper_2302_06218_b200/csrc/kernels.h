@@ -39,20 +39,19 @@ struct LocalAttnArgs {
   int kv_split = 1;
   void* out2 = nullptr;
   float* lse2 = nullptr;
+  // Fault injection only (DMHA_FAULT=perturb_lse, dmha.h): added to the
+  // partial's lse inside the log-sum-exp combine; 0 in normal operation.
+  float lse_bias = 0.f;
 };
 
-// bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu): picks
-// the variant per head dim (DMHA_KERNEL=pingpong|cluster|pair overrides).
+// bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu): two
+// query tiles per CTA, ping-pong on the tensor core.
 cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream);
-// Two query tiles per CTA, ping-pong on the tensor core (attn_fwd_sm100_v1.cu).
-cudaError_t launch_attn_fwd_bf16_pingpong(const LocalAttnArgs& a, cudaStream_t stream);
 // Whether launch_attn_fwd_bf16 accepts OUT_COMBINE_* for head dim D (the
 // ping-pong kernel with the one-thread-per-row epilogue does).
 bool attn_fused_combine_supported(int D);
 // Whether launch_attn_fwd_bf16 accepts kv_split = 2 for head dim D.
 bool attn_kv_split_supported(int D);
-// 64-key tiles with double-buffered scores (attn_fwd_sm100_v2.cu, "dbuf").
-cudaError_t launch_attn_fwd_bf16_dbuf(const LocalAttnArgs& a, cudaStream_t stream);
 // fp32 path (attn_fwd_fp32.cu).
 cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
 // log-sum-exp combine (lse_combine.cu).  out_dtype_bf16 selects the final
@@ -60,7 +59,7 @@ cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
 cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part,
                                const float* lse_part, void* out, float* lse_out, int64_t Lq,
                                int D, int H, int final_step, int out_dtype_bf16,
-                               cudaStream_t stream);
+                               cudaStream_t stream, float lse_bias = 0.f);
 
 // Head-parallel exchange (the paper's all-to-all).
 struct HeadparGeom {

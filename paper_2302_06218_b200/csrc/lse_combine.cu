@@ -25,6 +25,10 @@
 namespace dmha {
 namespace {
 
+// Every iteration is warp-uniform (the index space is rounded up to whole
+// warps) so the __syncwarp between the lse_acc reads of a row's lanes and the
+// lead lane's in-place write is executed by the full warp.  A row's D/4 lanes
+// (16 or 32) always sit in one warp: blocks start at multiples of 256 lanes.
 template <int D, bool kFinal, bool kBf16>
 __global__ void __launch_bounds__(256) lse_combine_kernel(float* __restrict__ o_acc,
                                                           float* __restrict__ lse_acc,
@@ -32,24 +36,30 @@ __global__ void __launch_bounds__(256) lse_combine_kernel(float* __restrict__ o_
                                                           const float* __restrict__ lse_part,
                                                           void* __restrict__ out,
                                                           float* __restrict__ lse_out,
-                                                          int64_t Lq, int H) {
+                                                          int64_t Lq, int H, float lse_bias) {
   constexpr int kVecPerRow = D / 4;
   const int64_t n_vec = Lq * H * kVecPerRow;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_vec;
+  const int64_t n_pad = (n_vec + 31) & ~static_cast<int64_t>(31);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_pad;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const bool ok = i < n_vec;
     const int64_t rh = i / kVecPerRow;  // (row, head) pair in [L, H] order
     const int64_t row = rh / H;
     const int head = static_cast<int>(rh - row * H);
     const int64_t li = static_cast<int64_t>(head) * Lq + row;
-    float wa, wp, lnew;
-    merge_weights(lse_acc[li], lse_part[li], wa, wp, lnew);
-    const float4 a = reinterpret_cast<const float4*>(o_acc)[i];
-    const float4 b = reinterpret_cast<const float4*>(o_part)[i];
-    float4 r;
-    r.x = combine_one(a.x, b.x, wa, wp);
-    r.y = combine_one(a.y, b.y, wa, wp);
-    r.z = combine_one(a.z, b.z, wa, wp);
-    r.w = combine_one(a.w, b.w, wa, wp);
+    float wa = 0.f, wp = 0.f, lnew = 0.f;
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) {
+      merge_weights(lse_acc[li], lse_part[li] + lse_bias, wa, wp, lnew);
+      const float4 a = reinterpret_cast<const float4*>(o_acc)[i];
+      const float4 b = reinterpret_cast<const float4*>(o_part)[i];
+      r.x = combine_one(a.x, b.x, wa, wp);
+      r.y = combine_one(a.y, b.y, wa, wp);
+      r.z = combine_one(a.z, b.z, wa, wp);
+      r.w = combine_one(a.w, b.w, wa, wp);
+    }
+    __syncwarp();  // every lane of the row has read lse_acc[li] before it is rewritten
+    if (!ok) continue;
     const bool lead = (i - rh * kVecPerRow) == 0;
     if (kFinal) {
       if (kBf16) {
@@ -73,7 +83,7 @@ __global__ void __launch_bounds__(256) lse_combine_kernel(float* __restrict__ o_
 template <int D>
 cudaError_t launch_d(float* o_acc, float* lse_acc, const float* o_part, const float* lse_part,
                      void* out, float* lse_out, int64_t Lq, int H, int final_step, int bf16,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, float bias) {
   const int64_t n_vec = Lq * H * (D / 4);
   int64_t blocks = (n_vec + 255) / 256;
   const int64_t cap = 148 * 8;  // 8 resident 256-thread blocks per SM, grid-strided
@@ -82,13 +92,13 @@ cudaError_t launch_d(float* o_acc, float* lse_acc, const float* o_part, const fl
   const unsigned g = static_cast<unsigned>(blocks);
   if (!final_step)
     lse_combine_kernel<D, false, false><<<g, 256, 0, stream>>>(o_acc, lse_acc, o_part, lse_part,
-                                                                out, lse_out, Lq, H);
+                                                                out, lse_out, Lq, H, bias);
   else if (bf16)
     lse_combine_kernel<D, true, true><<<g, 256, 0, stream>>>(o_acc, lse_acc, o_part, lse_part,
-                                                              out, lse_out, Lq, H);
+                                                              out, lse_out, Lq, H, bias);
   else
     lse_combine_kernel<D, true, false><<<g, 256, 0, stream>>>(o_acc, lse_acc, o_part, lse_part,
-                                                               out, lse_out, Lq, H);
+                                                               out, lse_out, Lq, H, bias);
   return cudaGetLastError();
 }
 
@@ -97,14 +107,14 @@ cudaError_t launch_d(float* o_acc, float* lse_acc, const float* o_part, const fl
 cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part,
                                const float* lse_part, void* out, float* lse_out, int64_t Lq,
                                int D, int H, int final_step, int out_dtype_bf16,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, float lse_bias) {
   if (Lq <= 0) return cudaSuccess;
   if (D == 64)
     return launch_d<64>(o_acc, lse_acc, o_part, lse_part, out, lse_out, Lq, H, final_step,
-                        out_dtype_bf16, stream);
+                        out_dtype_bf16, stream, lse_bias);
   if (D == 128)
     return launch_d<128>(o_acc, lse_acc, o_part, lse_part, out, lse_out, Lq, H, final_step,
-                         out_dtype_bf16, stream);
+                         out_dtype_bf16, stream, lse_bias);
   return cudaErrorInvalidValue;
 }
 

@@ -28,7 +28,7 @@ EXPORTED_SYMBOLS = (
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
     "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
     "dmha_forward_headpar", "dmha_forward_headpar_emulated", "dmha_mha_forward",
-    "dmha_select", "dmha_scatter_rows",
+    "dmha_select", "dmha_scatter_rows", "dmha_ring_workspace_bytes",
 )
 
 
@@ -44,7 +44,8 @@ class Stats(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_uint64), ("attn_launches", ctypes.c_uint64),
                 ("combine_launches", ctypes.c_uint64), ("exchanges", ctypes.c_uint64),
                 ("attn_ms", ctypes.c_double), ("combine_ms", ctypes.c_double),
-                ("exchange_ms", ctypes.c_double)]
+                ("exchange_ms", ctypes.c_double), ("last_bytes_sent", ctypes.c_uint64),
+                ("last_exchanges", ctypes.c_uint64)]
 
 
 class RingPlan(ctypes.Structure):
@@ -77,6 +78,7 @@ def lib():
             "dmha_forward_host": [P, P, P, P, P, I64, I, I, I],
             "dmha_forward_emulated": [I, I, P, P, P, P, P, I64, I, I, I],
             "dmha_workspace_bytes": [I64, I, I, ctypes.POINTER(SZ)],
+            "dmha_ring_workspace_bytes": [I, I64, I, I, ctypes.POINTER(SZ)],
             "dmha_get_stats": [ctypes.POINTER(Stats)],
             "dmha_local_to_global": [I64, I, I, I, I64, ctypes.POINTER(I64)],
             "dmha_attention_local": [P, P, P, P, P, I64, I64, I, I, I, I64, I64, I64, I64, I64, I64, I],
@@ -110,6 +112,45 @@ def _ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+_STATE = {"dtype": None}  # dtype given to init() (the library fixes it per process)
+
+
+def _need(cond: bool, msg: str):
+    if not cond:
+        raise DmhaError(ERR_INVALID, msg)
+
+
+def _check_tensors(tensors: dict, shapes: dict, dtypes: dict, device=None, pinned: bool = False):
+    """Argument checks the kernels rely on (they assume contiguous rows of
+    H*D elements and write exactly the documented sizes): every tensor is
+    contiguous, has the expected shape and dtype, and lives on one CUDA
+    device (or in host memory for the host path)."""
+    dev = None
+    for name, t in tensors.items():
+        if t is None:
+            continue
+        _need(t.is_contiguous(), f"{name} must be contiguous (got strides {tuple(t.stride())})")
+        if name in shapes:
+            _need(tuple(t.shape) == tuple(shapes[name]),
+                  f"{name} has shape {tuple(t.shape)}, expected {tuple(shapes[name])}")
+        if name in dtypes:
+            _need(t.dtype == dtypes[name], f"{name} has dtype {t.dtype}, expected {dtypes[name]}")
+        if pinned:
+            _need(t.device.type == "cpu", f"{name} must be a host tensor for the host path")
+        else:
+            _need(t.is_cuda, f"{name} must be a CUDA tensor")
+            if dev is None:
+                dev = t.device
+            _need(t.device == dev, f"{name} is on {t.device}, other arguments on {dev}")
+
+
+def _elem_dtype():
+    import torch
+    d = _STATE["dtype"]
+    _need(d is not None, "dmha.init() has not been called")
+    return torch.bfloat16 if d == BF16 else torch.float32
+
+
 def _cur_stream() -> int:
     import torch
     return int(torch.cuda.current_stream().cuda_stream)
@@ -141,6 +182,7 @@ def init(world_size: int = 1, rank: int = 0, unique_id: bytes | None = None, dev
     s = _cur_stream() if stream is None else int(stream)
     _check(lib().dmha_init(world_size, rank, None if uid is None else ctypes.addressof(uid), device,
                            dtype_code(dtype), layout_code(layout), s))
+    _STATE["dtype"] = dtype_code(dtype)
 
 
 def init_distributed(dtype="bf16", layout="contiguous", device: int | None = None):
@@ -163,6 +205,7 @@ def set_stream(stream: int):
 
 def finalize():
     _check(lib().dmha_finalize())
+    _STATE["dtype"] = None
 
 
 def synchronize():
@@ -177,6 +220,10 @@ def forward(q, k, v, L: int, causal: bool = False, out=None, lse=None):
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty((H, Lloc), dtype=torch.float32, device=q.device)
+    et = _elem_dtype()
+    _check_tensors(dict(q=q, k=k, v=v, out=out, lse=lse),
+                   dict(k=q.shape, v=q.shape, out=q.shape, lse=(H, Lloc)),
+                   dict(q=et, k=et, v=et, out=et, lse=torch.float32))
     set_stream(_cur_stream())
     _check(lib().dmha_forward(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
                               int(bool(causal))))
@@ -192,6 +239,10 @@ def forward_host(q, k, v, L: int, causal: bool = False, out=None, lse=None):
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty((H, Lloc), dtype=torch.float32, pin_memory=q.is_pinned())
+    et = _elem_dtype()
+    _check_tensors(dict(q=q, k=k, v=v, out=out, lse=lse),
+                   dict(k=q.shape, v=q.shape, out=q.shape, lse=(H, Lloc)),
+                   dict(q=et, k=et, v=et, out=et, lse=torch.float32), pinned=True)
     set_stream(_cur_stream())
     _check(lib().dmha_forward_host(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
                                    int(bool(causal))))
@@ -203,11 +254,15 @@ def forward_emulated(world_size: int, layout, q, k, v, L: int, causal: bool = Fa
     """Single-GPU emulation of the P-rank ring; q/k/v are [P, L/P, H, D] device tensors."""
     import torch
     P, Lloc, H, D = q.shape
-    assert P == world_size
+    _need(P == world_size, f"q has {P} shards, world_size {world_size}")
     if out is None:
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty((P, H, Lloc), dtype=torch.float32, device=q.device)
+    et = _elem_dtype()
+    _check_tensors(dict(q=q, k=k, v=v, out=out, lse=lse),
+                   dict(k=q.shape, v=q.shape, out=q.shape, lse=(P, H, Lloc)),
+                   dict(q=et, k=et, v=et, out=et, lse=torch.float32))
     set_stream(_cur_stream())
     _check(lib().dmha_forward_emulated(world_size, layout_code(layout), _ptr(q), _ptr(k), _ptr(v),
                                        _ptr(out), _ptr(lse), int(L), D, H, int(bool(causal))))
@@ -223,6 +278,10 @@ def forward_headpar(q, k, v, L: int, causal: bool = False, out=None, lse=None):
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty((H, Lloc), dtype=torch.float32, device=q.device)
+    et = _elem_dtype()
+    _check_tensors(dict(q=q, k=k, v=v, out=out, lse=lse),
+                   dict(k=q.shape, v=q.shape, out=q.shape, lse=(H, Lloc)),
+                   dict(q=et, k=et, v=et, out=et, lse=torch.float32))
     set_stream(_cur_stream())
     _check(lib().dmha_forward_headpar(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
                                       int(bool(causal))))
@@ -234,11 +293,15 @@ def forward_headpar_emulated(world_size: int, layout, q, k, v, L: int, causal: b
     """Single-GPU emulation of forward_headpar; q/k/v are [P, L/P, H, D]."""
     import torch
     P, Lloc, H, D = q.shape
-    assert P == world_size
+    _need(P == world_size, f"q has {P} shards, world_size {world_size}")
     if out is None:
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty((P, H, Lloc), dtype=torch.float32, device=q.device)
+    et = _elem_dtype()
+    _check_tensors(dict(q=q, k=k, v=v, out=out, lse=lse),
+                   dict(k=q.shape, v=q.shape, out=q.shape, lse=(P, H, Lloc)),
+                   dict(q=et, k=et, v=et, out=et, lse=torch.float32))
     set_stream(_cur_stream())
     _check(lib().dmha_forward_headpar_emulated(world_size, layout_code(layout), _ptr(q), _ptr(k),
                                                _ptr(v), _ptr(out), _ptr(lse), int(L), D, H,
@@ -253,6 +316,11 @@ def mha_forward(x, wq, wk, wv, wo, L: int, H: int, D: int, causal: bool = False,
     Lloc, d_model = x.shape
     if y is None:
         y = torch.empty((Lloc, d_model), dtype=x.dtype, device=x.device)
+    bf = torch.bfloat16
+    _check_tensors(dict(x=x, wq=wq, wk=wk, wv=wv, wo=wo, y=y, lse=lse),
+                   dict(wq=(d_model, H * D), wk=(d_model, H * D), wv=(d_model, H * D),
+                        wo=(H * D, d_model), y=(Lloc, d_model), lse=(H, Lloc)),
+                   dict(x=bf, wq=bf, wk=bf, wv=bf, wo=bf, y=bf, lse=torch.float32))
     set_stream(_cur_stream())
     _check(lib().dmha_mha_forward(_ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(y), _ptr(lse),
                                   int(L), int(d_model), int(D), int(H), int(bool(causal))))
@@ -311,9 +379,14 @@ def scatter_rows(y_sel, idx, y_full):
     return y_full
 
 
-def workspace_bytes(L: int, D: int, H: int) -> int:
+def workspace_bytes(L: int, D: int, H: int, world_size: int | None = None) -> int:
+    """Library workspace of a forward (dmha_workspace_bytes; with world_size,
+    dmha_ring_workspace_bytes — what forward_emulated at that size holds)."""
     n = ctypes.c_size_t(0)
-    _check(lib().dmha_workspace_bytes(int(L), D, H, ctypes.byref(n)))
+    if world_size is None:
+        _check(lib().dmha_workspace_bytes(int(L), D, H, ctypes.byref(n)))
+    else:
+        _check(lib().dmha_ring_workspace_bytes(int(world_size), int(L), D, H, ctypes.byref(n)))
     return n.value
 
 
@@ -348,20 +421,15 @@ def ring_plan(world_size: int, rank: int, step: int, layout, L: int) -> dict:
 
 
 def global_rows(L: int, world_size: int, rank: int, layout) -> np.ndarray:
-    """Global positions of rank `rank`'s local rows (vectorised form of
-    dmha_local_to_global; tests check the two agree)."""
-    lay = layout_code(layout)
-    P = world_size
-    if lay == ZIGZAG:
-        if L % (2 * P):
-            raise DmhaError(ERR_INVALID, f"L={L} not divisible by 2P={2 * P}")
-        c = L // (2 * P)
-        return np.concatenate([np.arange(rank * c, (rank + 1) * c),
-                               np.arange((2 * P - 1 - rank) * c, (2 * P - rank) * c)])
-    if L % P:
-        raise DmhaError(ERR_INVALID, f"L={L} not divisible by P={P}")
-    n = L // P
-    return np.arange(rank * n, (rank + 1) * n)
+    """Global positions of rank `rank`'s local rows, from the library's own
+    position map (the q map of dmha_ring_plan_step: two increasing pieces,
+    i < chunk -> base0 + i, else base1 + i - chunk; tests check it against
+    dmha_local_to_global row by row)."""
+    pl = ring_plan(world_size, rank, 0, layout, L)
+    n = L // world_size
+    c = pl["q_chunk"]
+    return np.concatenate([np.arange(pl["q_base0"], pl["q_base0"] + min(c, n)),
+                           np.arange(pl["q_base1"], pl["q_base1"] + max(0, n - c))]).astype(np.int64)
 
 
 def shard(x, world_size: int, rank: int, layout):

@@ -92,15 +92,40 @@ def test_c3_ring_p4_contiguous(oracle_mod):
     _check(out, lse, q, k, v, False, rows, oracle_mod, "C3 ring P=4")
 
 
-def test_c5_ring_p8_zigzag_causal(oracle_mod):
+@pytest.fixture(scope="module")
+def c5_inputs():
+    """C5 (BASELINE.json configs[4]): L=2^20, D=64, H=16, bf16-valued fp32 on
+    the host (the oracle's input) and bf16 on the device."""
+    L, H, D = 1 << 20, 16, 64
+    q, k, v = inputs.qkv(L, H, D, seed=1238)
+    return L, q, k, v
+
+
+def test_c5_ring_p8_zigzag_causal(oracle_mod, c5_inputs):
     """C5: L=2^20, D=64, H=16, causal, P=8 zigzag shards (emulated ring) — the
     million-scale configuration of BASELINE.json."""
-    L, H, D, P = 1 << 20, 16, 64, 8
-    q, k, v = inputs.qkv(L, H, D, seed=1238)
+    L, q, k, v = c5_inputs
+    P = 8
     out, lse = _ring_emulated(P, "zigzag", _to_dev(q), _to_dev(k), _to_dev(v), L, True)
     chunk = L // (2 * P)
     rows = _rows(L, [c * chunk for c in range(1, 2 * P)], 16, 96, seed=5)
     _check(out, lse, q, k, v, True, rows, oracle_mod, "C5 ring P=8 zigzag")
+
+
+def test_c5_p1_one_launch(oracle_mod, c5_inputs):
+    """C5 at N = 1 exactly as bench.py's secondary C5 line and the max-L runs
+    time it: ONE dmha_forward over all 2^20 keys (a single TMEM accumulator per
+    row, no ring combine).  Sampled rows: the first and last 64, both sides of
+    the 256-row CTA boundaries at every 2^16 rows (the zigzag chunk size at
+    P = 8) and of the last CTAs, and seeded random rows."""
+    L, q, k, v = c5_inputs
+    dq, dk, dv = _to_dev(q), _to_dev(k), _to_dev(v)
+    out, lse = dmha.forward(dq, dk, dv, L, True)
+    torch.cuda.synchronize()
+    del dq, dk, dv
+    bounds = [c * (1 << 16) for c in range(1, 16)] + [L - 256, L - 512]
+    rows = _rows(L, bounds, 8, 128, seed=6)
+    _check(out, lse, q, k, v, True, rows, oracle_mod, "C5 P=1 one launch")
 
 
 def test_64bit_offsets_large_q(oracle_mod):

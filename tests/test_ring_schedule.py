@@ -162,3 +162,23 @@ def test_plan_structure_and_bytes():
                     b = dmha.ring_plan(P, r, s + 1, layout, L)
                     assert b["compute_buf"] == a["recv_buf"]
                     assert b["src"] == (a["src"] - 1) % P
+
+
+def test_bench_gpus2_launches_two_ranks():
+    """bench.py --gpus 2 without a torchrun environment re-launches itself
+    under torch.distributed.run with two ranks (the driver's plain
+    `python bench.py --gpus N` invocation); --launch-check makes every rank
+    report and exit before touching a GPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--launch-check"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 and d["gpus"] == 2 for d in lines)
