@@ -7,11 +7,13 @@
 // time: lane t computes the full dot product of key j0+t (q row held in
 // registers), the chunk max / sum are warp-shuffle reductions, and each lane
 // accumulates D/32 output columns with the broadcast probabilities.
-// (A 3xTF32 tcgen05 variant is the planned replacement.)
+// The default fp32 path is the 3xTF32 tensor-core kernel (attn_fwd_tf32.cu);
+// this SIMT kernel is the independent cross-check behind DMHA_FP32_SIMT=1.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -111,6 +113,8 @@ __global__ void __launch_bounds__(256) attn_fwd_fp32_kernel(const float* __restr
 }  // namespace
 
 cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream) {
+  const char* e = std::getenv("DMHA_FP32_SIMT");
+  if (!(e && std::atoi(e) != 0)) return launch_attn_fwd_tf32x3(a, stream);
   if (a.Lq <= 0) return cudaSuccess;
   const int64_t warps = a.Lq * a.H;
   const int64_t blocks = (warps * 32 + 255) / 256;

@@ -63,17 +63,30 @@ struct Roles {
 };
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
 
-template <int D>
+// kPS (D = 128 only): P_g(j) goes to shared memory instead of over S_g's TMEM
+// columns, so QK^T(j+1) can run during softmax(j) (the separate-P schedule of
+// D = 64, whose P fits in TMEM).  Shared memory then holds Q (2 tiles), ONE K
+// slot, two V slots and the two P tiles: 224 KB of the 227 KB.
+template <int D, bool kPS>
 struct Cfg {
   static constexpr int kPanels = D / 64;                    // 128-byte swizzle panels per row
   static constexpr int kPanelBytes = 128 * 128;             // 128 rows x 128 B
   static constexpr int kTileBytes = kPanels * kPanelBytes;  // one 128 x D bf16 tile
-  static constexpr int kStages = (D == 128) ? 4 : 6;        // K/V ring slots
+  // Separate-P schedule: K and V in their own rings (kKSt / kVSt slots);
+  // otherwise one K/V ring of kStages slots (K_j, V_j alternate).
+  static constexpr bool kSepP = (D == 64) || kPS;
+  static constexpr int kKSt = (D == 64) ? 3 : 1;
+  static constexpr int kVSt = (D == 64) ? 3 : 2;
+  static constexpr int kStages = kSepP ? kKSt + kVSt : 4;
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = 2 * kTileBytes;
-  static constexpr int kRedOff = kKVOff + kStages * kTileBytes;  // split softmax: [2][2][2][128] f32 + l [2][2][128]
-  static constexpr int kBarOff = kRedOff + 12 * 128 * 4;
+  static constexpr int kPOff = kKVOff + kStages * kTileBytes;     // kPS: P_0, P_1 (128 x 128 bf16)
+  static constexpr int kRedOff = kPOff + (kPS ? 2 * 128 * 128 * 2 : 0);
+  // split softmax: [2][2][2][128] f32 row maxima + l [2][2][128]
+  static constexpr int kRedBytes = kPS ? 0 : 12 * 128 * 4;
+  static constexpr int kBarOff = kRedOff + kRedBytes;
   static constexpr int kSmemBytes = kBarOff + 256 + 1024;   // + barriers + align slack
+  static_assert(kSmemBytes <= 232448, "shared memory budget (227 KB)");
   static constexpr uint32_t kIdescQK = ptx::make_idesc(1, kBM, kBN, 0, 0);
   static constexpr uint32_t kIdescPV = ptx::make_idesc(1, kBM, D, 0, 1);  // V is MN-major
 };
@@ -140,23 +153,26 @@ __device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
   return static_cast<int>((lim + kBN - 1) / kBN);
 }
 
-template <int D, int kEmu, bool kSplit, int kIss>
+template <int D, int kEmu, bool kSplit, int kIss, bool kPS>
 __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const Params p) {
-  using C = Cfg<D>;
+  using C = Cfg<D, kPS>;
   using R = Roles<kSplit>;
   constexpr int kProducerWarp = R::kProducerWarp;
   constexpr int kMmaWarp = R::kMmaWarp;
-  // D = 64: separate P buffers (TMEM has room) decouple S_g(j+1) from PV_g(j).
-  constexpr bool kSepP = (D == 64);
+  // Separate P buffers decouple S_g(j+1) from PV_g(j): in TMEM for D = 64
+  // (room next to O_g), in shared memory for D = 128 (kPS).
+  constexpr bool kSepP = C::kSepP;
+  static_assert(!kPS || (D == 128 && !kSplit), "P in shared memory: D = 128, one warpgroup per tile");
   constexpr uint32_t kPCol = 256 + 64;  // P_g at kPCol + 128 g (D = 64 only)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem + C::kQOff;
   uint8_t* sKV = smem + C::kKVOff;
+  uint8_t* sP = smem + C::kPOff;  // kPS only
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;
@@ -190,9 +206,13 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     ptx::mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
-      // one release per issuer that reads the slot (kIss = 4: V slots — the odd
-      // ones, kStages is even — are read by both PV issuers)
-      ptx::mbar_init(&kv_empty[s], (kIss == 2 || (kIss == 4 && (s & 1))) ? 2 : 1);
+      // one release per issuer that reads the slot: separate-P rings hold K in
+      // slots [0, kKSt) (read by the S issuers) and V after them (read by the
+      // PV issuers; two for kIss = 2 and 4); the single ring is read by every
+      // issuer
+      const bool v_slot = kSepP && s >= C::kKSt;
+      const int readers = kSepP ? ((kIss == 2 || (kIss == 4 && v_slot)) ? 2 : 1) : (kIss == 2 ? 2 : 1);
+      ptx::mbar_init(&kv_empty[s], readers);
     }
     for (int g = 0; g < 2; ++g) {
       ptx::mbar_init(&s_full[g], 1);
@@ -220,19 +240,39 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         for (int pn = 0; pn < C::kPanels; ++pn)
           ptx::tma_load_3d(&tm_q, q_full, sQ + g * C::kTileBytes + pn * C::kPanelBytes, pn * 64,
                            head, static_cast<int32_t>(m0 + g * kBM));
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int j = 0; j < nkv; ++j) {
-        for (int which = 0; which < 2; ++which) {
-          trace_x(p, 5 + 9 * which, j);
-          ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
-          trace_x(p, 6 + 9 * which, j);
-          ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
-          const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
-          for (int pn = 0; pn < C::kPanels; ++pn)
-            ptx::tma_load_3d(tm, &kv_full[stage], sKV + stage * C::kTileBytes + pn * C::kPanelBytes,
-                             pn * 64, head, (jt0 + j) * kBN);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      if constexpr (kSepP) {
+        // K_j -> K ring slot j % kKSt, V_j -> V ring slot j % kVSt (separate
+        // rings: K_{j+1} only waits for S(j), not for PV(j-1))
+        for (int j = 0; j < nkv; ++j) {
+          for (int which = 0; which < 2; ++which) {
+            const int nst = which == 0 ? C::kKSt : C::kVSt;
+            const int slot = (which == 0 ? 0 : C::kKSt) + j % nst;
+            const uint32_t ph = static_cast<uint32_t>((j / nst) & 1);
+            trace_x(p, 5 + 9 * which, j);
+            ptx::mbar_wait(&kv_empty[slot], ph ^ 1);
+            trace_x(p, 6 + 9 * which, j);
+            ptx::mbar_arrive_expect_tx(&kv_full[slot], C::kTileBytes);
+            const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
+            for (int pn = 0; pn < C::kPanels; ++pn)
+              ptx::tma_load_3d(tm, &kv_full[slot], sKV + slot * C::kTileBytes + pn * C::kPanelBytes,
+                               pn * 64, head, (jt0 + j) * kBN);
+          }
+        }
+      } else {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int j = 0; j < nkv; ++j) {
+          for (int which = 0; which < 2; ++which) {
+            trace_x(p, 5 + 9 * which, j);
+            ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+            trace_x(p, 6 + 9 * which, j);
+            ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
+            const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
+            for (int pn = 0; pn < C::kPanels; ++pn)
+              ptx::tma_load_3d(tm, &kv_full[stage], sKV + stage * C::kTileBytes + pn * C::kPanelBytes,
+                               pn * 64, head, (jt0 + j) * kBN);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
@@ -254,13 +294,22 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       };
       // D = 64: P_g lives at columns [320 + 128g, 384 + 128g) (the unused half
       // of O_g's 128-column slot).
+      // D = 128 with kPS: P_g is a 128 x 128 bf16 K-major tile in shared
+      // memory (the 128-byte-swizzled layout TMA gives Q), an SS MMA operand.
+      const uint32_t sp = ptx::smem_u32(sP);
       auto pv_sep = [&](int g, int slot, bool acc) {
         const uint32_t b0 = skv + slot * C::kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          ptx::mma_bf16_ts(tmem + 256 + g * 128, tmem + kPCol + g * 128 + kk * 8,
-                           ptx::smem_desc_sw128(b0 + kk * 16 * 128, C::kPanelBytes, 1024),
-                           C::kIdescPV, (acc || kk > 0) ? 1u : 0u);
+          const uint64_t bdesc = ptx::smem_desc_sw128(b0 + kk * 16 * 128, C::kPanelBytes, 1024);
+          if constexpr (kPS) {
+            const uint32_t a0 = sp + g * (kBM * kBN * 2) + (kk >> 2) * C::kPanelBytes + (kk & 3) * 32;
+            ptx::mma_bf16_ss(tmem + 256 + g * 128, ptx::smem_desc_sw128(a0, 16, 1024), bdesc,
+                             C::kIdescPV, (acc || kk > 0) ? 1u : 0u);
+          } else {
+            ptx::mma_bf16_ts(tmem + 256 + g * 128, tmem + kPCol + g * 128 + kk * 8, bdesc,
+                             C::kIdescPV, (acc || kk > 0) ? 1u : 0u);
+          }
         }
       };
       auto pv = [&](int g, int slot, bool acc) {
@@ -280,61 +329,61 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         // issues A-from-TMEM MMAs at only ~69 cycles each whatever N is
         // (tools/umma_multi.cu: two issuers reach 39, the N = 64 PV needs 32),
         // and each Q tile's chain no longer waits behind the other's barriers.
-        // K/V ring item i: K_t = item 2t, V_t = item 2t+1 (load order); every
-        // slot is released by both issuers (kv_empty count 2).
+        // K_t sits in K ring slot t % kKSt, V_t in V ring slot kKSt + t % kVSt
+        // (separate rings, see the producer); each slot is released by every
+        // issuer that reads it (kv_empty counts).
         // kIss = 1: one thread issues both Q tiles (S0 S1, then PV0 PV1);
         // kIss = 2: warp kMmaWarp + g issues Q tile g (S_g and PV_g);
         // kIss = 3: warp kMmaWarp issues S0 S1, warp kMmaWarp + 1 PV0 PV1.
         // kIss = 4: warp kMmaWarp issues S0 S1, warp kMmaWarp + 1 + g PV_g.
-        static_assert(C::kStages % 2 == 0, "K and V must keep their slot parity");
         const int role = warp - kMmaWarp;
         const int g_lo = kIss == 2 ? role : (kIss == 4 && role > 0 ? role - 1 : 0);
         const int g_hi = (kIss == 2 || (kIss == 4 && role > 0)) ? g_lo + 1 : 2;
         const bool do_s = (kIss != 3 && kIss != 4) || role == 0;
         const bool do_pv = (kIss != 3 && kIss != 4) || role >= 1;
-        auto slot_of = [](int item) { return item % C::kStages; };
-        auto par_of = [](int item) { return static_cast<uint32_t>((item / C::kStages) & 1); };
+        auto kslot = [](int t) { return t % C::kKSt; };
+        auto kpar = [](int t) { return static_cast<uint32_t>((t / C::kKSt) & 1); };
+        auto vslot = [](int t) { return C::kKSt + t % C::kVSt; };
+        auto vpar = [](int t) { return static_cast<uint32_t>((t / C::kVSt) & 1); };
         ptx::mbar_wait(q_full, 0);
         if (do_s) {
-          ptx::mbar_wait(&kv_full[slot_of(0)], par_of(0));
+          ptx::mbar_wait(&kv_full[kslot(0)], kpar(0));
           ptx::tc_fence_after();
           for (int g = g_lo; g < g_hi; ++g) {
-            qk(g, slot_of(0));
+            qk(g, kslot(0));
             ptx::mma_commit(&s_full[g]);
           }
-          ptx::mma_commit(&kv_empty[slot_of(0)]);
+          ptx::mma_commit(&kv_empty[kslot(0)]);
         }
         for (int j = 1; j <= nkv; ++j) {
           const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
           if (do_s && j < nkv) {  // S_g(j): needs K_j and S_g(j-1) consumed
-            const int ik = 2 * j;
             trace_x(p, 9 * g_lo + 0, j);
-            ptx::mbar_wait(&kv_full[slot_of(ik)], par_of(ik));
+            ptx::mbar_wait(&kv_full[kslot(j)], kpar(j));
             trace_x(p, 9 * g_lo + 1, j);
             for (int g = g_lo; g < g_hi; ++g) {
               ptx::mbar_wait(&s_free[g], ppar);
               if (g == g_lo) trace_x(p, 9 * g_lo + 2, j);
               ptx::tc_fence_after();
-              qk(g, slot_of(ik));
+              qk(g, kslot(j));
               ptx::mma_commit(&s_full[g]);
             }
             if (g_lo == 0) trace_stamp(p, 6, j);
-            ptx::mma_commit(&kv_empty[slot_of(ik)]);
+            ptx::mma_commit(&kv_empty[kslot(j)]);
           }
-          if (do_pv) {
-            const int iv = 2 * (j - 1) + 1;  // V_{j-1}
-            ptx::mbar_wait(&kv_full[slot_of(iv)], par_of(iv));
+          if (do_pv) {  // PV_g(j-1): needs V_{j-1} and P_g(j-1)
+            ptx::mbar_wait(&kv_full[vslot(j - 1)], vpar(j - 1));
             trace_x(p, 9 * g_lo + 3, j - 1);
             for (int g = g_lo; g < g_hi; ++g) {
               ptx::mbar_wait(&p_ready[g], ppar);
               trace_stamp(p, 4 + g, j - 1);
               ptx::tc_fence_after();
-              pv_sep(g, slot_of(iv), j > 1);
+              pv_sep(g, vslot(j - 1), j > 1);
               ptx::mma_commit(&pv_done[g]);
               if (j == nkv) ptx::mma_commit(&o_final[g]);
             }
             trace_x(p, 9 * g_lo + 4, j - 1);
-            ptx::mma_commit(&kv_empty[slot_of(iv)]);
+            ptx::mma_commit(&kv_empty[vslot(j - 1)]);
           }
         }
       } else if constexpr (kIss == 2) {
@@ -676,7 +725,12 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
           ptx::tc_fence_after();
         }
-        l_run += sm::store_p(s, tP);
+        if constexpr (kPS) {
+          l_run += sm::store_p_smem(s, sP + g * (kBM * kBN * 2), r);
+          ptx::fence_proxy_async_smem();
+        } else {
+          l_run += sm::store_p(s, tP);
+        }
       } else if (kEmu == 0 || masked) {
         // scalar FFMA + MUFU.EX2 (the measured-fastest form on B200)
         float sum0 = 0.f, sum1 = 0.f;
@@ -695,8 +749,6 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           ptx::tmem_st16(tP + c * 16, pk);
         }
         l_run += sum0 + sum1;
-      } else if (kEmu == 8) {
-        l_run += sm::exp_tile_2pass(s, sl2, m_use, tP);
       } else {
         l_run += sm::exp_tile<kEmu>(s, sl2, m_use, tP);
       }
@@ -811,9 +863,9 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
-template <int D, int E, bool S, int I = 2>
+template <int D, int E, bool S, int I = 2, bool PS = false>
 cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
-  using C = Cfg<D>;
+  using C = Cfg<D, PS>;
   CUtensorMap tq, tk, tv;
   if (!make_tma_map_bf16(&tq, a.q, a.Lq, a.H, D, kBM) || !make_tma_map_bf16(&tk, a.k, a.Lk, a.H, D, kBN) ||
       !make_tma_map_bf16(&tv, a.v, a.Lk, a.H, D, kBN))
@@ -823,7 +875,7 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   int cur_dev = 0;
   cudaGetDevice(&cur_dev);
   if (attr_dev != cur_dev) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, S, I>,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, E, S, I, PS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -849,7 +901,7 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.lse_bias = a.lse_bias;
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H, p.kv_split);
-  attn_fwd_sm100_kernel<D, E, S, I><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
+  attn_fwd_sm100_kernel<D, E, S, I, PS><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
@@ -858,22 +910,35 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
 //  DMHA_EMU     = pairs (of every 8) of score columns on the FMA-pipe exp2 (0)
 //  DMHA_ISSUERS = MMA-issuing threads: 1 = one for both Q tiles (D = 128
 //                 default), 2 = one per Q tile (D = 64 split-softmax
-//                 default), 3 = split S / PV issuers (D = 64 only; default of
-//                 the two-warpgroup D = 64 kernel), 4 = S issuer + one PV
-//                 issuer per Q tile (D = 64 only)
+//                 default), 3 = split S / PV issuers, 4 = S issuer + one PV
+//                 issuer per Q tile (3 and 4: separate-P schedules only)
 //  DMHA_SPLIT   = 1: split-row softmax (16 softmax warps; D = 64 default)
+//  DMHA_PS      = 1: D = 128 with P in shared memory (separate-P schedule)
 struct PingpongConfig {
   bool split;
   int iss;
+  bool ps;
 };
 PingpongConfig pingpong_config(int D) {
   // D = 64 default: the split softmax (16 softmax warps, two per row) with one
   // MMA issuer per Q tile (DESIGN.md §5 lessons 16-17)
-  PingpongConfig c{D == 64, 1};
+  PingpongConfig c{D == 64, 1, false};
   if (const char* e = std::getenv("DMHA_SPLIT")) c.split = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DMHA_PS")) c.ps = D == 128 && std::atoi(e) != 0;
+  if (c.ps) c.split = false;
   c.iss = D == 64 ? (c.split ? 2 : 3) : 1;
   if (const char* e = std::getenv("DMHA_ISSUERS")) c.iss = std::atoi(e);
   return c;
+}
+
+template <int D, bool S, int I, bool PS = false>
+cudaError_t launch_emu(int emu, const LocalAttnArgs& a, cudaStream_t stream) {
+  switch (emu) {
+    case 1: return launch_de<D, 1, S, I, PS>(a, stream);
+    case 2: return launch_de<D, 2, S, I, PS>(a, stream);
+    case 3: return launch_de<D, 3, S, I, PS>(a, stream);
+    default: return launch_de<D, 0, S, I, PS>(a, stream);
+  }
 }
 
 template <int D>
@@ -882,46 +947,34 @@ cudaError_t launch_d(const LocalAttnArgs& a, cudaStream_t stream) {
   if (const char* e = std::getenv("DMHA_EMU")) emu = std::atoi(e);
   const PingpongConfig cfg = pingpong_config(D);
   const int iss = cfg.iss;
-  const bool split = cfg.split;
-  if (split) {
-    if (iss == 2) {
-      if constexpr (D == 64) {  // FMA-pipe exp2 offload (DMHA_EMU pairs of every 8)
-        switch (emu) {
-          case 1: return launch_de<D, 1, true, 2>(a, stream);
-          case 2: return launch_de<D, 2, true, 2>(a, stream);
-          case 3: return launch_de<D, 3, true, 2>(a, stream);
-          default: break;
-        }
+  if constexpr (D == 128) {
+    if (cfg.ps) {  // separate-P schedule, P in shared memory
+      switch (iss) {
+        case 2: return launch_emu<D, false, 2, true>(emu, a, stream);
+        case 3: return launch_de<D, 0, false, 3, true>(a, stream);
+        case 4: return launch_de<D, 0, false, 4, true>(a, stream);
+        default: return launch_emu<D, false, 1, true>(emu, a, stream);
       }
+    }
+  }
+  if (cfg.split) {
+    if (iss == 2) {
+      if constexpr (D == 64) return launch_emu<D, true, 2>(emu, a, stream);
       return launch_de<D, 0, true, 2>(a, stream);
     }
-    if (D == 64 && iss == 4) return launch_de<D, 0, true, 4>(a, stream);
-    if (D == 64 && iss == 3) {
-      switch (emu) {
-        case 1: return launch_de<D, 1, true, 3>(a, stream);
-        case 2: return launch_de<D, 2, true, 3>(a, stream);
-        default: return launch_de<D, 0, true, 3>(a, stream);
-      }
+    if constexpr (D == 64) {
+      if (iss == 4) return launch_de<D, 0, true, 4>(a, stream);
+      if (iss == 3) return launch_emu<D, true, 3>(emu, a, stream);
     }
     if (a.out_mode >= OUT_COMBINE_ACC) return cudaErrorInvalidValue;  // see pingpong_fused_combine_ok
     return launch_de<D, 0, true, 1>(a, stream);
   }
-  if (iss == 2) return emu == 1 ? launch_de<D, 1, false, 2>(a, stream)
-                                : launch_de<D, 0, false, 2>(a, stream);
-  if (D == 64 && iss == 4) return launch_de<D, 0, false, 4>(a, stream);
-  if (D == 64 && iss == 3) {
-    switch (emu) {
-      case 1: return launch_de<D, 1, false, 3>(a, stream);
-      case 2: return launch_de<D, 2, false, 3>(a, stream);
-      default: return launch_de<D, 0, false, 3>(a, stream);
-    }
+  if (iss == 2) return launch_emu<D, false, 2>(emu, a, stream);
+  if constexpr (D == 64) {
+    if (iss == 4) return launch_de<D, 0, false, 4>(a, stream);
+    if (iss == 3) return launch_emu<D, false, 3>(emu, a, stream);
   }
-  switch (emu) {
-    case 1: return launch_de<D, 1, false, 1>(a, stream);
-    case 2: return launch_de<D, 2, false, 1>(a, stream);
-    case 8: return launch_de<D, 8, false, 1>(a, stream);  // two-pass exponentials
-    default: return launch_de<D, 0, false, 1>(a, stream);
-  }
+  return launch_emu<D, false, 1>(emu, a, stream);
 }
 
 }  // namespace
@@ -933,7 +986,7 @@ bool pingpong_fused_combine_ok(int D) {
   // it runs with per-tile or split issuers (the D = 64 configurations).  The
   // D = 128 split softmax (single issuer) keeps the separate combine pass.
   const PingpongConfig c = pingpong_config(D);
-  return !c.split || (D == 64 && (c.iss == 2 || c.iss == 3));
+  return c.ps || !c.split || (D == 64 && (c.iss == 2 || c.iss == 3));
 }
 
 bool attn_fused_combine_supported(int D) {

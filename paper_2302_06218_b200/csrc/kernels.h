@@ -52,8 +52,10 @@ cudaError_t launch_attn_fwd_bf16(const LocalAttnArgs& a, cudaStream_t stream);
 bool attn_fused_combine_supported(int D);
 // Whether launch_attn_fwd_bf16 accepts kv_split = 2 for head dim D.
 bool attn_kv_split_supported(int D);
-// fp32 path (attn_fwd_fp32.cu).
+// fp32 path: the 3xTF32 tcgen05 kernel (attn_fwd_tf32.cu), or with
+// DMHA_FP32_SIMT=1 the SIMT fp32 kernel (attn_fwd_fp32.cu).
 cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
+cudaError_t launch_attn_fwd_tf32x3(const LocalAttnArgs& a, cudaStream_t stream);
 // log-sum-exp combine (lse_combine.cu).  out_dtype_bf16 selects the final
 // output element type when final_step != 0.
 cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part,

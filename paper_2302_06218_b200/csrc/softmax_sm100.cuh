@@ -174,6 +174,35 @@ __device__ __forceinline__ float store_p(const float (&s)[128], uint32_t tP) {
   return t.x + t.y;
 }
 
+// Pass 2 for P in shared memory (D = 128, kPS): pack the 128 exponentials of
+// row r to bf16 and store them as row r of a 128 x 128 K-major tile in the
+// 128-byte-swizzled layout an SS MMA operand descriptor (SWIZZLE_128B) reads
+// — two 64-key panels of 128 rows x 128 B, 16-byte chunk c of row r stored
+// at chunk c ^ (r & 7) — with 16 vector stores (a warp's 32 rows of one chunk
+// take the minimum 4 wavefronts).  Returns the fp32 sum.  The caller fences
+// (fence.proxy.async) before signalling the MMA issuer.
+__device__ __forceinline__ float store_p_smem(const float (&s)[128], uint8_t* tile, int r) {
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                   make_float2(0.f, 0.f)};
+  uint8_t* row = tile + r * 128;
+  const int sw = r & 7;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 pe = make_float2(s[8 * c + 2 * t], s[8 * c + 2 * t + 1]);
+      acc[t] = __fadd2_rn(acc[t], pe);
+      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
+      w[t] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    *reinterpret_cast<uint4*>(row + (c >> 3) * (128 * 128) + (((c & 7) ^ sw) << 4)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  const float2 t = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+  return t.x + t.y;
+}
+
 // Half-row versions (64 columns, split softmax): exponentials in place, then
 // pack + store 32 P columns at tP and return the fp32 sum.
 template <int EMU = 0>  // EMU of every 8 column pairs on the FMA-pipe polynomial (finite inputs)
