@@ -82,6 +82,16 @@ struct dmha_stats {
    * blocks).  Ring: exactly (P-1) * 2 * L_loc*H*D*elem per rank. */
   uint64_t last_bytes_sent;
   uint64_t last_exchanges;
+  /* Profiling only: the head-parallel exchange's pack/unpack copy kernels
+   * (NEXT-1), CUDA-event time summed, and the bytes they read + wrote. */
+  uint64_t pack_launches;
+  double pack_ms;
+  uint64_t pack_bytes;
+  /* Profiling only: the NEXT-3 projection GEMMs (dmha_linear, tcgen05),
+   * CUDA-event time summed and their algorithmic FLOP (2*M*N*K each). */
+  uint64_t gemm_launches;
+  double gemm_ms;
+  double gemm_flop;
 };
 
 /* ---- setup / teardown ----------------------------------------------------
@@ -175,12 +185,22 @@ int dmha_forward_headpar(const void *q, const void *k, const void *v, void *out,
  *  wq, wk, wv: DEVICE [d_model, H*D] bf16 row-major (head h = columns
  *  [h*D, (h+1)*D)); wo: DEVICE [H*D, d_model]; y: DEVICE [L_loc, d_model] bf16;
  *  lse: DEVICE [H, L_loc] fp32 or NULL.  bf16 dtype only; d_model % 8 == 0.
- * The projections are plain cuBLAS bf16 GEMMs (fp32 accumulate); Q, K, V and
- * O are kept as bf16 activations in library workspace (reading R17).
- * Collective like dmha_forward. */
+ * The projections are dmha_linear (hand-written tcgen05 GEMMs, fp32
+ * accumulate); Q, K, V and O are kept as bf16 activations in library
+ * workspace (reading R17).  Collective like dmha_forward. */
 int dmha_mha_forward(const void *x, const void *wq, const void *wk, const void *wv,
                      const void *wo, void *y, float *lse, int64_t L, int d_model, int D, int H,
                      int causal);
+
+/* NEXT-3 projection step (PAPER.md:186-191 V = X W^V, K = X W^K, Q = X W^Q;
+ * P:675 the W_0 projection): y = x w on this rank, row-major bf16,
+ *  x: DEVICE [M, K], w: DEVICE [K, N], y: DEVICE [M, N] (caller-owned, fully
+ *  overwritten, must not overlap x or w); fp32 accumulation on the tcgen05
+ *  tensor cores (TMEM), bf16 round-to-nearest-even output.
+ * N and K positive multiples of 8 (16-byte rows), M >= 0 (M = 0 is a no-op),
+ * 16-byte aligned pointers; bf16 dtype only (DMHA_ERR_UNSUPPORTED otherwise).
+ * Asynchronous on the library stream; no communication (rows are local). */
+int dmha_linear(const void *x, const void *w, void *y, int64_t M, int N, int K);
 
 /* Single-GPU emulation of dmha_forward_headpar at world size P (buffers as in
  * dmha_forward_emulated); the all-to-alls become device copies. */

@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdmha.so"
 OBJ = PKG / "build"
-SOURCES = ["attn_fwd_sm100.cu", "attn_fwd_tf32.cu", "attn_fwd_fp32.cu", "lse_combine.cu", "headpar.cu", "selector.cu", "dmha_api.cu"]
+SOURCES = ["attn_fwd_sm100.cu", "attn_fwd_tf32.cu", "attn_fwd_fp32.cu", "lse_combine.cu", "headpar.cu", "selector.cu", "gemm_sm100.cu", "dmha_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -30,12 +30,6 @@ def nccl_root() -> Path:
     if not (p / "include" / "nccl.h").exists():
         raise RuntimeError(f"nccl headers not found under {p}")
     return p
-
-
-def cublas_root() -> Path:
-    """cuBLAS of the nvidia wheel torch uses (same soname, loaded once)."""
-    purelib = Path(sysconfig.get_paths()["purelib"])
-    return purelib / "nvidia" / "cublas"
 
 
 def nvcc() -> str:
@@ -77,10 +71,9 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> Path:
     if LIB.exists() and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
         return LIB
     nr = nccl_root()
-    cb = cublas_root()
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", *map(str, objs), "-o", str(LIB),
-           "-L", str(nr / "lib"), "-l:libnccl.so.2", "-L", str(cb / "lib"), "-l:libcublas.so.12",
-           "-Xlinker", f"-rpath={nr / 'lib'}", "-Xlinker", f"-rpath={cb / 'lib'}"]
+           "-L", str(nr / "lib"), "-l:libnccl.so.2",
+           "-Xlinker", f"-rpath={nr / 'lib'}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

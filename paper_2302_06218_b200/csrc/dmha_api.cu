@@ -15,7 +15,6 @@
 //   compute:         attention(q_r, kv_s, positions of src) -> partial;
 //                    s = 0 writes the accumulator, s >= 1 combines into it, the
 //                    last step writes out/lse.  P = 1 writes out/lse directly.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
@@ -82,12 +81,11 @@ struct State {
   // head-parallel exchange workspace (dmha_forward_headpar*)
   void* hp = nullptr;
   size_t hp_bytes = 0;
-  // NEXT-3 layer workspace (dmha_mha_forward): q, k, v, o, lse; cuBLAS handle
+  // NEXT-3 layer workspace (dmha_mha_forward): q, k, v, o, lse
   void* mha = nullptr;
   size_t mha_bytes = 0;
   void* sel = nullptr;  // NEXT-4 selector workspace
   size_t sel_bytes = 0;
-  cublasHandle_t blas = nullptr;
   // host-path staging
   void* st_qkv = nullptr;  // q, k, v back to back
   void* st_out = nullptr;
@@ -102,7 +100,9 @@ struct State {
   bool profile = false;
   struct Rec {
     cudaEvent_t a, b;
-    int kind;  // 0 attention, 1 combine, 2 exchange
+    int kind;  // 0 attention, 1 combine, 2 exchange, 3 head-parallel pack/unpack, 4 GEMM
+    uint64_t bytes;
+    double flop = 0.0;
   };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
@@ -123,13 +123,13 @@ cudaEvent_t pool_event() {
 
 // Bracket the launches enqueued by `fn` on `stream` with profiling events.
 template <typename F>
-int timed(int kind, cudaStream_t stream, F&& fn) {
+int timed(int kind, cudaStream_t stream, F&& fn, uint64_t bytes = 0) {
   if (!g.profile) return fn();
   cudaEvent_t a = pool_event(), b = pool_event();
   if (a) cudaEventRecord(a, stream);
   int rc = fn();
   if (b) cudaEventRecord(b, stream);
-  if (a && b) g.pending.push_back({a, b, kind});
+  if (a && b) g.pending.push_back({a, b, kind, bytes, 0.0});
   return rc;
 }
 
@@ -143,6 +143,14 @@ void resolve_profiles() {
       } else if (r.kind == 1) {
         g.stats.combine_ms += ms;
         g.stats.combine_launches++;
+      } else if (r.kind == 4) {
+        g.stats.gemm_ms += ms;
+        g.stats.gemm_launches++;
+        g.stats.gemm_flop += r.flop;
+      } else if (r.kind == 3) {
+        g.stats.pack_ms += ms;
+        g.stats.pack_launches++;
+        g.stats.pack_bytes += r.bytes;
       } else {
         g.stats.exchange_ms += ms;
         g.stats.exchanges++;
@@ -646,6 +654,23 @@ int ensure_hp(size_t bytes) {
     g.stats.kernel_launches++;                                                            \
   } while (0)
 
+// A head-parallel pack/unpack launch, timed as kind 3 when profiling; `bytes`
+// = the bytes it reads + writes (algorithmic, for the GB/s roofline).
+#define CK_PACK(expr, bytes)                                                                \
+  do {                                                                                      \
+    cudaError_t _pe = cudaSuccess;                                                          \
+    timed(3, g.stream, [&]() { _pe = (expr); return 0; }, (bytes));                         \
+    if (_pe != cudaSuccess) return fail(DMHA_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_pe)); \
+    g.stats.kernel_launches++;                                                              \
+  } while (0)
+
+// Bytes one pack/unpack kernel moves (read + write): the Q/K/V shuffles copy
+// 3 * L_loc*H*D elements, the output shuffles L_loc*H*D (+ the fp32 lse).
+uint64_t hp_qkv_bytes(int64_t Lloc, int H, int D, size_t e) { return 2ull * 3 * Lloc * H * D * e; }
+uint64_t hp_out_bytes(int64_t Lloc, int H, int D, size_t e, bool with_lse) {
+  return 2ull * Lloc * H * (D * e + (with_lse ? 4 : 0));
+}
+
 // One rank's head-parallel forward; `ws` is this rank's workspace (layout y).
 template <typename Ex1, typename Ex2>
 int headpar_rank(int P, int r, int layout, const void* q, const void* k, const void* v,
@@ -656,22 +681,26 @@ int headpar_rank(int P, int r, int layout, const void* q, const void* k, const v
   const int64_t Lloc = L / P;
   const int e = static_cast<int>(elem_bytes(g.dtype));
   const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
-  CK_LAUNCH(dmha::launch_headpar_pack_qkv(q, k, v, ws + y.send1, geo, e, g.stream));
+  CK_PACK(dmha::launch_headpar_pack_qkv(q, k, v, ws + y.send1, geo, e, g.stream),
+          hp_qkv_bytes(Lloc, H, D, e));
   if (int rc = exchange_qkv()) return rc;
-  CK_LAUNCH(dmha::launch_headpar_unpack_qkv(ws + y.recv1, ws + y.xq, ws + y.xk, ws + y.xv, geo,
-                                            e, g.stream));
+  CK_PACK(dmha::launch_headpar_unpack_qkv(ws + y.recv1, ws + y.xq, ws + y.xk, ws + y.xv, geo,
+                                          e, g.stream),
+          hp_qkv_bytes(Lloc, H, D, e));
   const dmha::PosMap full{0, L, L};
   if (int rc = run_local(ws + y.xq, ws + y.xk, ws + y.xv, ws + y.outg,
                          reinterpret_cast<float*>(ws + y.lseg), L, L, D, H / P, causal, full, full,
                          dmha::OUT_FINAL))
     return rc;
-  CK_LAUNCH(dmha::launch_headpar_pack_out(ws + y.outg, ws + y.send2,
-                                          reinterpret_cast<const float*>(ws + y.lseg),
-                                          reinterpret_cast<float*>(ws + y.send_lse), geo, e,
-                                          g.stream));
+  CK_PACK(dmha::launch_headpar_pack_out(ws + y.outg, ws + y.send2,
+                                        reinterpret_cast<const float*>(ws + y.lseg),
+                                        reinterpret_cast<float*>(ws + y.send_lse), geo, e,
+                                        g.stream),
+          hp_out_bytes(Lloc, H, D, e, true));
   if (do_exchange_out_now) {
     if (int rc = exchange_out()) return rc;
-    CK_LAUNCH(dmha::launch_headpar_unpack_out(ws + y.recv2, out, geo, e, g.stream));
+    CK_PACK(dmha::launch_headpar_unpack_out(ws + y.recv2, out, geo, e, g.stream),
+            hp_out_bytes(Lloc, H, D, e, false));
   }
   (void)lse;
   return DMHA_OK;
@@ -767,7 +796,6 @@ int dmha_finalize(void) {
   free_ptr(g.sel);
   free_ptr(g.hp);
   free_ptr(g.mha);
-  if (g.blas) cublasDestroy(g.blas);
   resolve_profiles();
   for (cudaEvent_t e : g.pool) cudaEventDestroy(e);
   g.pool.clear();
@@ -814,6 +842,8 @@ int dmha_set_profiling(int enable) {
   g.profile = enable != 0;
   g.stats.attn_launches = g.stats.combine_launches = g.stats.exchanges = 0;
   g.stats.attn_ms = g.stats.combine_ms = g.stats.exchange_ms = 0.0;
+  g.stats.pack_launches = g.stats.pack_bytes = g.stats.gemm_launches = 0;
+  g.stats.pack_ms = g.stats.gemm_ms = g.stats.gemm_flop = 0.0;
   return DMHA_OK;
 }
 
@@ -1087,10 +1117,11 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
   // Phase 1: every rank packs; the all-to-all is P*P device copies.
   for (int r = 0; r < P; ++r) {
     const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
-    CK_LAUNCH(dmha::launch_headpar_pack_qkv(static_cast<const char*>(q) + r * shard,
-                                            static_cast<const char*>(k) + r * shard,
-                                            static_cast<const char*>(v) + r * shard,
-                                            ws_of(r) + y.send1, geo, static_cast<int>(e), g.stream));
+    CK_PACK(dmha::launch_headpar_pack_qkv(static_cast<const char*>(q) + r * shard,
+                                          static_cast<const char*>(k) + r * shard,
+                                          static_cast<const char*>(v) + r * shard,
+                                          ws_of(r) + y.send1, geo, static_cast<int>(e), g.stream),
+            hp_qkv_bytes(Lloc, H, D, e));
   }
   for (int s = 0; s < P; ++s)
     for (int d = 0; d < P; ++d) {
@@ -1103,17 +1134,19 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
     const int64_t Lg = L;
     const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
     char* ws = ws_of(r);
-    CK_LAUNCH(dmha::launch_headpar_unpack_qkv(ws + y.recv1, ws + y.xq, ws + y.xk, ws + y.xv, geo,
-                                              static_cast<int>(e), g.stream));
+    CK_PACK(dmha::launch_headpar_unpack_qkv(ws + y.recv1, ws + y.xq, ws + y.xk, ws + y.xv, geo,
+                                            static_cast<int>(e), g.stream),
+            hp_qkv_bytes(Lloc, H, D, e));
     const dmha::PosMap full{0, Lg, Lg};
     if (int rc = run_local(ws + y.xq, ws + y.xk, ws + y.xv, ws + y.outg,
                            reinterpret_cast<float*>(ws + y.lseg), Lg, Lg, D, H / P, causal, full,
                            full, dmha::OUT_FINAL))
       return rc;
-    CK_LAUNCH(dmha::launch_headpar_pack_out(ws + y.outg, ws + y.send2,
-                                            reinterpret_cast<const float*>(ws + y.lseg),
-                                            reinterpret_cast<float*>(ws + y.send_lse), geo,
-                                            static_cast<int>(e), g.stream));
+    CK_PACK(dmha::launch_headpar_pack_out(ws + y.outg, ws + y.send2,
+                                          reinterpret_cast<const float*>(ws + y.lseg),
+                                          reinterpret_cast<float*>(ws + y.send_lse), geo,
+                                          static_cast<int>(e), g.stream),
+            hp_out_bytes(Lloc, H, D, e, true));
   }
   (void)nothing;
   // Phase 3: all-to-all back (out blocks and lse blocks), unpack per rank.
@@ -1128,11 +1161,43 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
     }
   for (int r = 0; r < P; ++r) {
     const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
-    CK_LAUNCH(dmha::launch_headpar_unpack_out(ws_of(r) + y.recv2, static_cast<char*>(out) + r * shard,
-                                              geo, static_cast<int>(e), g.stream));
+    CK_PACK(dmha::launch_headpar_unpack_out(ws_of(r) + y.recv2, static_cast<char*>(out) + r * shard,
+                                            geo, static_cast<int>(e), g.stream),
+            hp_out_bytes(Lloc, H, D, e, false));
   }
   g.stats.forwards++;
   return DMHA_OK;
+}
+
+// NEXT-3 projection GEMM on the compute stream (timed as kind 4 when profiling).
+int run_gemm(const void* A, const void* B, void* C, int64_t M, int N, int K) {
+  cudaError_t e = cudaSuccess;
+  const auto t0 = g.pending.size();
+  timed(4, g.stream, [&]() {
+    e = dmha::launch_gemm_bf16(A, B, C, M, N, K, g.stream);
+    return 0;
+  });
+  if (g.pending.size() > t0) g.pending.back().flop = 2.0 * static_cast<double>(M) * N * K;
+  if (e != cudaSuccess)
+    return fail(DMHA_ERR_CUDA, "dmha: projection GEMM launch failed: %s", cudaGetErrorString(e));
+  g.stats.kernel_launches++;
+  return DMHA_OK;
+}
+
+int dmha_linear(const void* x, const void* w, void* y, int64_t M, int N, int K) {
+  if (int rc = check_state()) return rc;
+  if (g.dtype != DMHA_BF16) return fail(DMHA_ERR_UNSUPPORTED, "dmha_linear: bf16 only");
+  if (!x || !w || !y) return fail(DMHA_ERR_INVALID, "dmha_linear: null pointer");
+  if (M < 0 || N < 1 || K < 1 || N % 8 != 0 || K % 8 != 0 || M > INT32_MAX)
+    return fail(DMHA_ERR_INVALID, "dmha_linear: need M >= 0, N and K positive multiples of 8");
+  const void* ptrs[3] = {x, w, y};
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+      return fail(DMHA_ERR_INVALID, "dmha_linear: pointers must be 16-byte aligned");
+  const size_t yb = static_cast<size_t>(M) * N * 2;
+  if (overlaps(y, yb, x, static_cast<size_t>(M) * K * 2) || overlaps(y, yb, w, static_cast<size_t>(K) * N * 2))
+    return fail(DMHA_ERR_INVALID, "dmha_linear: y overlaps x or w");
+  return run_gemm(x, w, y, M, N, K);
 }
 
 int dmha_mha_forward(const void* x, const void* wq, const void* wk, const void* wv,
@@ -1158,10 +1223,6 @@ int dmha_mha_forward(const void* x, const void* wq, const void* wk, const void* 
     g.mha_bytes = need;
     update_ws_stat();
   }
-  if (!g.blas && cublasCreate(&g.blas) != CUBLAS_STATUS_SUCCESS)
-    return fail(DMHA_ERR_CUDA, "dmha_mha_forward: cublasCreate failed");
-  if (cublasSetStream(g.blas, g.stream) != CUBLAS_STATUS_SUCCESS)
-    return fail(DMHA_ERR_CUDA, "dmha_mha_forward: cublasSetStream failed");
   char* ws = static_cast<char*>(g.mha);
   char* q = ws;
   char* k = q + act;
@@ -1169,15 +1230,9 @@ int dmha_mha_forward(const void* x, const void* wq, const void* wk, const void* 
   char* o = v + act;
   float* l = reinterpret_cast<float*>(o + act);
   const int HD = H * D;
-  const float one = 1.f, zero = 0.f;
-  // Row-major C[M,N] = A[M,K] B[K,N]  <=>  column-major C^T = B^T A^T.
+  // Row-major C[M,N] = A[M,K] B[K,N] on the tcgen05 GEMM (gemm_sm100.cu).
   auto gemm = [&](const void* A, const void* B, void* Cm, int64_t M, int N, int K) -> int {
-    cublasStatus_t st = cublasGemmEx(g.blas, CUBLAS_OP_N, CUBLAS_OP_N, N, static_cast<int>(M), K,
-                                     &one, B, CUDA_R_16BF, N, A, CUDA_R_16BF, K, &zero, Cm,
-                                     CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-    if (st != CUBLAS_STATUS_SUCCESS)
-      return fail(DMHA_ERR_CUDA, "dmha_mha_forward: cublasGemmEx failed (%d)", static_cast<int>(st));
-    return DMHA_OK;
+    return run_gemm(A, B, Cm, M, N, K);
   };
   // replicated W_Q, W_K, W_V applied to this rank's rows, all heads.
   if (int rc = gemm(x, wq, q, Lloc, HD, d_model)) return rc;

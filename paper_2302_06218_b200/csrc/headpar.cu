@@ -7,8 +7,12 @@
 // one contiguous message, and scatter received rows to their GLOBAL positions
 // (which for the zigzag layout are not contiguous per rank).
 //
-// All kernels are HBM-bound copies: one thread moves 16 bytes; D * elem bytes
-// per (row, head) is a multiple of 16.
+// All kernels are HBM-bound copies.  The unit of work is one row SEGMENT: the
+// Hp = H/P heads of one (peer, tensor, row), Hp*D*elem contiguous bytes on
+// both sides (a multiple of 16).  One warp copies a segment with 16-byte
+// loads/stores; the (peer, tensor) pair comes from blockIdx.z / blockIdx.y and
+// the row from a warp-strided loop, so there is no per-element div/mod.
+// Algorithmic bytes: 2x the bytes moved (read + write), see DESIGN.md.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -18,6 +22,8 @@
 namespace dmha {
 namespace {
 
+constexpr int kWarps = 8;  // warps (= row segments in flight) per block
+
 __device__ __forceinline__ int64_t gpos(const HeadparGeom& g, int rank, int64_t i) {
   if (g.zigzag) {
     const int64_t c = g.Lloc / 2;
@@ -26,93 +32,78 @@ __device__ __forceinline__ int64_t gpos(const HeadparGeom& g, int rank, int64_t 
   return rank * g.Lloc + i;
 }
 
-// x_t [Lloc, H, D] (t = q, k, v) -> send [P(dest)][3][Lloc][Hp][D]
+__device__ __forceinline__ void copy_seg(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                         int n, int lane) {
+  for (int w = lane; w < n; w += 32) dst[w] = src[w];
+}
+
+// Warp-strided loop over the Lloc rows of this block's (peer, tensor).
+#define FOR_ROWS(i)                                                                     \
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);      \
+       i < g.Lloc; i += static_cast<int64_t>(gridDim.x) * kWarps)
+
+// x_t [Lloc, H, D] (t = q, k, v) -> send [P(dest)][3][Lloc][Hp][D];
+// blockIdx.z = dest d, blockIdx.y = t
 __global__ void pack_qkv_kernel(const uint4* __restrict__ q, const uint4* __restrict__ k,
                                 const uint4* __restrict__ v, uint4* __restrict__ send,
                                 HeadparGeom g, int vec) {
-  const int Hp = g.H / g.P;
-  const int64_t n = static_cast<int64_t>(g.P) * 3 * g.Lloc * Hp * vec;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t r = e;
-    const int w = static_cast<int>(r % vec); r /= vec;
-    const int hh = static_cast<int>(r % Hp); r /= Hp;
-    const int64_t i = r % g.Lloc; r /= g.Lloc;
-    const int t = static_cast<int>(r % 3); r /= 3;
-    const int d = static_cast<int>(r);
-    const uint4* src = t == 0 ? q : (t == 1 ? k : v);
-    send[e] = src[(i * g.H + d * Hp + hh) * vec + w];
-  }
+  const int Hp = g.H / g.P, seg = Hp * vec, lane = threadIdx.x & 31;
+  const int d = blockIdx.z, t = blockIdx.y;
+  const uint4* src = t == 0 ? q : (t == 1 ? k : v);
+  uint4* dst = send + (static_cast<int64_t>(d) * 3 + t) * g.Lloc * seg;
+  FOR_ROWS(i) copy_seg(dst + i * seg, src + (i * g.H + d * Hp) * vec, seg, lane);
 }
 
-// recv [P(src)][3][Lloc][Hp][D] -> X_t [L, Hp, D] in global row order
+// recv [P(src)][3][Lloc][Hp][D] -> X_t [L, Hp, D] in global row order;
+// blockIdx.z = source s, blockIdx.y = t
 __global__ void unpack_qkv_kernel(const uint4* __restrict__ recv, uint4* __restrict__ xq,
                                   uint4* __restrict__ xk, uint4* __restrict__ xv, HeadparGeom g,
                                   int vec) {
-  const int Hp = g.H / g.P;
-  const int64_t n = static_cast<int64_t>(g.P) * 3 * g.Lloc * Hp * vec;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t r = e;
-    const int w = static_cast<int>(r % vec); r /= vec;
-    const int hh = static_cast<int>(r % Hp); r /= Hp;
-    const int64_t i = r % g.Lloc; r /= g.Lloc;
-    const int t = static_cast<int>(r % 3); r /= 3;
-    const int s = static_cast<int>(r);
-    uint4* dst = t == 0 ? xq : (t == 1 ? xk : xv);
-    dst[(gpos(g, s, i) * Hp + hh) * vec + w] = recv[e];
-  }
+  const int Hp = g.H / g.P, seg = Hp * vec, lane = threadIdx.x & 31;
+  const int s = blockIdx.z, t = blockIdx.y;
+  uint4* dst = t == 0 ? xq : (t == 1 ? xk : xv);
+  const uint4* src = recv + (static_cast<int64_t>(s) * 3 + t) * g.Lloc * seg;
+  FOR_ROWS(i) copy_seg(dst + gpos(g, s, i) * seg, src + i * seg, seg, lane);
 }
 
-// out_g [L, Hp, D] (global order) -> send [P(dest)][Lloc][Hp][D]; lse_g [Hp, L] ->
-// send_lse [P(dest)][Hp][Lloc]
+// out_g [L, Hp, D] (global order) -> send [P(dest)][Lloc][Hp][D] (blockIdx.y = 0);
+// lse_g [Hp, L] -> send_lse [P(dest)][Hp][Lloc] (blockIdx.y = 1, thread per row)
 __global__ void pack_out_kernel(const uint4* __restrict__ outg, uint4* __restrict__ send,
                                 const float* __restrict__ lseg, float* __restrict__ send_lse,
                                 HeadparGeom g, int vec) {
-  const int Hp = g.H / g.P;
-  const int64_t n = static_cast<int64_t>(g.P) * g.Lloc * Hp * vec;
-  const int64_t nl = static_cast<int64_t>(g.P) * Hp * g.Lloc;
-  const int64_t L = g.Lloc * g.P;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n + nl;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (e < n) {
-      int64_t r = e;
-      const int w = static_cast<int>(r % vec); r /= vec;
-      const int hh = static_cast<int>(r % Hp); r /= Hp;
-      const int64_t i = r % g.Lloc; r /= g.Lloc;
-      const int d = static_cast<int>(r);
-      send[e] = outg[(gpos(g, d, i) * Hp + hh) * vec + w];
-    } else {
-      int64_t r = e - n;
-      const int64_t i = r % g.Lloc; r /= g.Lloc;
-      const int hh = static_cast<int>(r % Hp); r /= Hp;
-      const int d = static_cast<int>(r);
-      send_lse[e - n] = lseg[hh * L + gpos(g, d, i)];
+  const int Hp = g.H / g.P, seg = Hp * vec, lane = threadIdx.x & 31;
+  const int d = blockIdx.z;
+  if (blockIdx.y == 0) {
+    uint4* dst = send + static_cast<int64_t>(d) * g.Lloc * seg;
+    FOR_ROWS(i) copy_seg(dst + i * seg, outg + gpos(g, d, i) * seg, seg, lane);
+  } else {
+    const int64_t L = g.Lloc * g.P;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < g.Lloc;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t gp = gpos(g, d, i);
+      for (int hh = 0; hh < Hp; ++hh)
+        send_lse[(static_cast<int64_t>(d) * Hp + hh) * g.Lloc + i] = lseg[hh * L + gp];
     }
   }
 }
 
-// recv [P(src)][Lloc][Hp][D] -> out [Lloc, H, D] (head block of src)
+// recv [P(src)][Lloc][Hp][D] -> out [Lloc, H, D] (head block of src); blockIdx.z = s
 __global__ void unpack_out_kernel(const uint4* __restrict__ recv, uint4* __restrict__ out,
                                   HeadparGeom g, int vec) {
-  const int Hp = g.H / g.P;
-  const int64_t n = static_cast<int64_t>(g.P) * g.Lloc * Hp * vec;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t r = e;
-    const int w = static_cast<int>(r % vec); r /= vec;
-    const int hh = static_cast<int>(r % Hp); r /= Hp;
-    const int64_t i = r % g.Lloc; r /= g.Lloc;
-    const int s = static_cast<int>(r);
-    out[(i * g.H + s * Hp + hh) * vec + w] = recv[e];
-  }
+  const int Hp = g.H / g.P, seg = Hp * vec, lane = threadIdx.x & 31;
+  const int s = blockIdx.z;
+  const uint4* src = recv + static_cast<int64_t>(s) * g.Lloc * seg;
+  FOR_ROWS(i) copy_seg(out + (i * g.H + s * Hp) * vec, src + i * seg, seg, lane);
 }
+#undef FOR_ROWS
 
-unsigned grid_for(int64_t n) {
-  int64_t b = (n + 255) / 256;
-  const int64_t cap = 148 * 8;
-  if (b > cap) b = cap;
-  return static_cast<unsigned>(b < 1 ? 1 : b);
+// About 8 resident blocks per SM over the whole (x, y, z) grid.
+dim3 grid_for(const HeadparGeom& g, int planes_y) {
+  const int64_t planes = static_cast<int64_t>(g.P) * planes_y;
+  int64_t bx = (g.Lloc + kWarps - 1) / kWarps;
+  const int64_t cap = (148 * 8 + planes - 1) / planes;
+  if (bx > cap) bx = cap;
+  return dim3(static_cast<unsigned>(bx < 1 ? 1 : bx), planes_y, g.P);
 }
 
 }  // namespace
@@ -120,21 +111,18 @@ unsigned grid_for(int64_t n) {
 cudaError_t launch_headpar_pack_qkv(const void* q, const void* k, const void* v, void* send,
                                     const HeadparGeom& g, int elem_bytes, cudaStream_t st) {
   const int vec = g.D * elem_bytes / 16;
-  const int64_t n = static_cast<int64_t>(g.P) * 3 * g.Lloc * (g.H / g.P) * vec;
-  pack_qkv_kernel<<<grid_for(n), 256, 0, st>>>(static_cast<const uint4*>(q),
-                                                static_cast<const uint4*>(k),
-                                                static_cast<const uint4*>(v),
-                                                static_cast<uint4*>(send), g, vec);
+  pack_qkv_kernel<<<grid_for(g, 3), 32 * kWarps, 0, st>>>(
+      static_cast<const uint4*>(q), static_cast<const uint4*>(k), static_cast<const uint4*>(v),
+      static_cast<uint4*>(send), g, vec);
   return cudaGetLastError();
 }
 
 cudaError_t launch_headpar_unpack_qkv(const void* recv, void* xq, void* xk, void* xv,
                                       const HeadparGeom& g, int elem_bytes, cudaStream_t st) {
   const int vec = g.D * elem_bytes / 16;
-  const int64_t n = static_cast<int64_t>(g.P) * 3 * g.Lloc * (g.H / g.P) * vec;
-  unpack_qkv_kernel<<<grid_for(n), 256, 0, st>>>(static_cast<const uint4*>(recv),
-                                                  static_cast<uint4*>(xq), static_cast<uint4*>(xk),
-                                                  static_cast<uint4*>(xv), g, vec);
+  unpack_qkv_kernel<<<grid_for(g, 3), 32 * kWarps, 0, st>>>(
+      static_cast<const uint4*>(recv), static_cast<uint4*>(xq), static_cast<uint4*>(xk),
+      static_cast<uint4*>(xv), g, vec);
   return cudaGetLastError();
 }
 
@@ -142,18 +130,16 @@ cudaError_t launch_headpar_pack_out(const void* outg, void* send, const float* l
                                     float* send_lse, const HeadparGeom& g, int elem_bytes,
                                     cudaStream_t st) {
   const int vec = g.D * elem_bytes / 16;
-  const int64_t n = static_cast<int64_t>(g.P) * g.Lloc * (g.H / g.P) * (vec + 1);
-  pack_out_kernel<<<grid_for(n), 256, 0, st>>>(static_cast<const uint4*>(outg),
-                                                static_cast<uint4*>(send), lseg, send_lse, g, vec);
+  pack_out_kernel<<<grid_for(g, 2), 32 * kWarps, 0, st>>>(
+      static_cast<const uint4*>(outg), static_cast<uint4*>(send), lseg, send_lse, g, vec);
   return cudaGetLastError();
 }
 
 cudaError_t launch_headpar_unpack_out(const void* recv, void* out, const HeadparGeom& g,
                                       int elem_bytes, cudaStream_t st) {
   const int vec = g.D * elem_bytes / 16;
-  const int64_t n = static_cast<int64_t>(g.P) * g.Lloc * (g.H / g.P) * vec;
-  unpack_out_kernel<<<grid_for(n), 256, 0, st>>>(static_cast<const uint4*>(recv),
-                                                  static_cast<uint4*>(out), g, vec);
+  unpack_out_kernel<<<grid_for(g, 1), 32 * kWarps, 0, st>>>(static_cast<const uint4*>(recv),
+                                                             static_cast<uint4*>(out), g, vec);
   return cudaGetLastError();
 }
 

@@ -63,6 +63,11 @@ cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part
                                int D, int H, int final_step, int out_dtype_bf16,
                                cudaStream_t stream, float lse_bias = 0.f);
 
+// NEXT-3 projection GEMM (gemm_sm100.cu): row-major bf16 C[M,N] = A[M,K] B[K,N],
+// fp32 accumulation; N % 8 == 0, K % 8 == 0.
+cudaError_t launch_gemm_bf16(const void* a, const void* b, void* c, int64_t M, int N, int K,
+                             cudaStream_t stream);
+
 // Head-parallel exchange (the paper's all-to-all).
 struct HeadparGeom {
   int P;         // world size

@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "dmha_forward", "dmha_forward_host", "dmha_forward_emulated", "dmha_workspace_bytes",
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
     "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
-    "dmha_forward_headpar", "dmha_forward_headpar_emulated", "dmha_mha_forward",
+    "dmha_forward_headpar", "dmha_forward_headpar_emulated", "dmha_mha_forward", "dmha_linear",
     "dmha_select", "dmha_scatter_rows", "dmha_ring_workspace_bytes",
 )
 
@@ -45,7 +45,10 @@ class Stats(ctypes.Structure):
                 ("combine_launches", ctypes.c_uint64), ("exchanges", ctypes.c_uint64),
                 ("attn_ms", ctypes.c_double), ("combine_ms", ctypes.c_double),
                 ("exchange_ms", ctypes.c_double), ("last_bytes_sent", ctypes.c_uint64),
-                ("last_exchanges", ctypes.c_uint64)]
+                ("last_exchanges", ctypes.c_uint64), ("pack_launches", ctypes.c_uint64),
+                ("pack_ms", ctypes.c_double), ("pack_bytes", ctypes.c_uint64),
+                ("gemm_launches", ctypes.c_uint64), ("gemm_ms", ctypes.c_double),
+                ("gemm_flop", ctypes.c_double)]
 
 
 class RingPlan(ctypes.Structure):
@@ -90,6 +93,7 @@ def lib():
             "dmha_forward_headpar": [P, P, P, P, P, I64, I, I, I],
             "dmha_forward_headpar_emulated": [I, I, P, P, P, P, P, I64, I, I, I],
             "dmha_mha_forward": [P, P, P, P, P, P, P, I64, I, I, I, I],
+            "dmha_linear": [P, P, P, I64, I, I],
             "dmha_select": [P, I64, I, I, P, ctypes.c_double, P, P, P, ctypes.POINTER(I64)],
             "dmha_scatter_rows": [P, P, I64, I, P],
         }
@@ -324,6 +328,20 @@ def mha_forward(x, wq, wk, wv, wo, L: int, H: int, D: int, causal: bool = False,
     set_stream(_cur_stream())
     _check(lib().dmha_mha_forward(_ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(y), _ptr(lse),
                                   int(L), int(d_model), int(D), int(H), int(bool(causal))))
+    return y
+
+
+def linear(x, w, y=None):
+    """NEXT-3 projection step y = x @ w (bf16 [M, K] x [K, N], tcgen05 GEMM)."""
+    import torch
+    M, K = x.shape
+    N = w.shape[1]
+    if y is None:
+        y = torch.empty((M, N), dtype=x.dtype, device=x.device)
+    bf = torch.bfloat16
+    _check_tensors(dict(x=x, w=w, y=y), dict(w=(K, N), y=(M, N)), dict(x=bf, w=bf, y=bf))
+    set_stream(_cur_stream())
+    _check(lib().dmha_linear(_ptr(x), _ptr(w), _ptr(y), int(M), int(N), int(K)))
     return y
 
 

@@ -2,8 +2,11 @@
 
     python tools/bench_steps.py [--out profiles/r01_steps.json]
 
-a2  attention kernel: TFLOP/s per config (C2, C2 causal, C3@P=1, C4@P=1, C5@P=1)
-    and per kernel variant, CUDA-event timed on the launch stream
+a2  attention kernel: TFLOP/s per config (C2, C2 causal, C3@P=1, C4@P=1, C5@P=1),
+    CUDA-event timed on the launch stream; the fp32 path (3xTF32) at C1 and
+    at C2's shape
+NEXT-1 head-parallel pack/unpack kernels: HBM GB/s (library profiling events)
+NEXT-3 projection GEMM (tcgen05): TFLOP/s at the layer's shapes
 a4  LSE combine kernel: HBM GB/s (12 B/elem + 12 B/row) at C4 P=8 shard size
 a1+a2+a4 through the single-GPU ring emulation (P = 2, 4, 8) at C3 size:
     the per-rank compute of the real ring without NCCL (the exchange step,
@@ -63,10 +66,7 @@ def main():
         q, k, v = (torch.randn(L, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
         out = torch.empty_like(q)
         lse = torch.empty(H, L, device="cuda")
-        for kern in ("pingpong", "cluster", "pair"):
-            if kern == "pair" and D != 128:
-                continue
-            os.environ["DMHA_KERNEL"] = kern
+        for kern in ("default",):
             iters = 2 if L >= 262144 else 10
             ms = time_cuda(lambda: dmha.forward(q, k, v, L, causal, out, lse), iters=iters, warmup=2)
             tf = attn_flops(L, D, H, causal) / ms / 1e9
@@ -75,7 +75,63 @@ def main():
                                         "frac_sustained": tf / PEAKS["bf16_tflops_sustained"],
                                         "frac_burst": tf / PEAKS["bf16_tflops"], "frac_datasheet": tf / 2250.0})
             print(json.dumps(res["a2_attention"][-1]), flush=True)
-        os.environ.pop("DMHA_KERNEL", None)
+        del q, k, v, out, lse
+        torch.cuda.empty_cache()
+
+    dmha.finalize()
+    # fp32 path (3xTF32 tcgen05): C1 and C2's shape in fp32
+    res["fp32_path"] = []
+    dmha.init(1, 0, None, 0, "fp32", "contiguous")
+    for name, L, D, H, causal in (("C1", 512, 64, 4, False), ("C2-fp32", 16384, 64, 8, False)):
+        q, k, v = (torch.randn(L, H, D, device="cuda") for _ in range(3))
+        out = torch.empty_like(q)
+        lse = torch.empty(H, L, device="cuda")
+        ms = time_cuda(lambda: dmha.forward(q, k, v, L, causal, out, lse), iters=10)
+        tf = attn_flops(L, D, H, causal) / ms / 1e9
+        rec = {"config": name, "L": L, "D": D, "H": H, "ms": ms, "tflops": tf,
+               "frac_tf32_datasheet_1125": tf / 1125.0,
+               "note": "3xTF32: 3 tensor-core passes per GEMM (counted once, algorithmic FLOP)"}
+        res["fp32_path"].append(rec)
+        print(json.dumps(rec), flush=True)
+    dmha.finalize()
+    dmha.init(1, 0, None, 0, "bf16", "contiguous")
+
+    # NEXT-3 projection GEMM: x [L_loc, d_model] @ W [d_model, H*D]
+    res["gemm"] = []
+    for M, N, K in ((32768, 2048, 2048), (131072, 2048, 2048), (262144, 2048, 2048), (16384, 1024, 1024)):
+        x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(K, N, device="cuda") / K ** 0.5).to(torch.bfloat16)
+        y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ms = time_cuda(lambda: dmha.linear(x, w, y), iters=20)
+        tf = 2.0 * M * N * K / ms / 1e9
+        ms_cb = time_cuda(lambda: torch.matmul(x, w, out=y), iters=20)
+        rec = {"M": M, "N": N, "K": K, "ms": ms, "tflops": tf,
+               "frac_sustained": tf / PEAKS["bf16_tflops_sustained"], "frac_burst": tf / PEAKS["bf16_tflops"],
+               "context_torch_matmul_tflops": 2.0 * M * N * K / ms_cb / 1e9}
+        res["gemm"].append(rec)
+        print(json.dumps(rec), flush=True)
+        del x, w, y
+
+    # NEXT-1 pack/unpack kernels (head-parallel exchange) at C4 P=8 / C5 P=8 shard sizes
+    res["headpar_pack"] = []
+    for L, D, H, P, layout in ((262144, 128, 16, 8, "contiguous"), (1 << 20, 64, 16, 8, "zigzag")):
+        Ll = L // P
+        q, k, v = (torch.randn(P, Ll, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
+        out = torch.empty_like(q)
+        lse = torch.empty(P, H, Ll, device="cuda")
+        dmha.forward_headpar_emulated(P, layout, q, k, v, L, layout == "zigzag", out, lse)
+        torch.cuda.synchronize()
+        dmha.set_profiling(True)
+        dmha.forward_headpar_emulated(P, layout, q, k, v, L, layout == "zigzag", out, lse)
+        torch.cuda.synchronize()
+        st = dmha.get_stats()
+        dmha.set_profiling(False)
+        gbs = st["pack_bytes"] / (st["pack_ms"] / 1e3) / 1e9
+        rec = {"L": L, "D": D, "H": H, "P": P, "layout": layout, "launches": st["pack_launches"],
+               "ms_total": st["pack_ms"], "bytes": st["pack_bytes"], "gbs": gbs,
+               "frac_hbm": gbs / PEAKS["hbm_gbs"]}
+        res["headpar_pack"].append(rec)
+        print(json.dumps(rec), flush=True)
         del q, k, v, out, lse
         torch.cuda.empty_cache()
 
