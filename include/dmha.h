@@ -197,7 +197,8 @@ int dmha_mha_forward(const void *x, const void *wq, const void *wk, const void *
  *  x: DEVICE [M, K], w: DEVICE [K, N], y: DEVICE [M, N] (caller-owned, fully
  *  overwritten, must not overlap x or w); fp32 accumulation on the tcgen05
  *  tensor cores (TMEM), bf16 round-to-nearest-even output.
- * N and K positive multiples of 8 (16-byte rows), M >= 0 (M = 0 is a no-op),
+ * N and K positive multiples of 8 (16-byte rows), M >= 0 (M = 0 is a no-op and
+ * accepts null x / y),
  * 16-byte aligned pointers; bf16 dtype only (DMHA_ERR_UNSUPPORTED otherwise).
  * Asynchronous on the library stream; no communication (rows are local). */
 int dmha_linear(const void *x, const void *w, void *y, int64_t M, int N, int K);

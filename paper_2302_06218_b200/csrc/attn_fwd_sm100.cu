@@ -107,6 +107,7 @@ struct Params {
   int kv_split;    // 1, or 2: blockIdx.z picks one half of each CTA's key tiles
   int n_mblk;
   float lse_bias;  // fault injection (DMHA_FAULT=perturb_lse): added to lse_s in the combine; 0
+  int spec;        // speculative max on the one-warpgroup-per-tile path (DMHA_SPEC, default 1)
   unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
 
@@ -519,35 +520,60 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 64; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
-      const float pmax = sm::row_max64(s);
+      // Row max without a barrier before the exponentials: each half takes
+      // m_loc = its own half's max when that exceeds the running max by more
+      // than the threshold (else the stale running max), publishes m_loc with
+      // a non-blocking bar.arrive, computes its exponentials, and only then
+      // reads the partner's m_loc (barrier (g, partner, tile parity), long
+      // satisfied by then).  Both halves end with the same row max
+      // m_row = max(m_loc, m_loc'); a half whose m_loc is below it scales its
+      // P by 2^(m_loc - m_row) <= 1 (rare).  Online-softmax state stays
+      // exact: l, O and P always share m_run.
+      const float own = sm::row_max64(s) * sl2;
+      const bool own_w = __any_sync(0xffffffffu, own > m_run + kRescaleThreshold);
+      const float m_loc = own_w ? fmaxf(m_run, own) : m_run;
       float* red_t = red + ((j & 1) * 2 + g) * 2 * kBM;
-      red_t[h * kBM + r] = pmax;
-      asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
-      const float mt = fmaxf(pmax, red_t[(h ^ 1) * kBM + r]) * sl2;
-      const bool need = mt > m_run + kRescaleThreshold;
-      const bool warp_rescale = __any_sync(0xffffffffu, need);  // same in both halves
-      float alpha = 1.f;
-      if (warp_rescale) {
-        const float m_new = fmaxf(m_run, mt);
-        alpha = (m_new == -INFINITY) ? 1.f : ptx::ex2_approx(m_run - m_new);
-        l_run *= alpha;
-        m_run = m_new;
+      red_t[h * kBM + r] = m_loc;
+      asm volatile("bar.arrive %0, 256;" ::"r"(3 + ((g * 2 + h) * 2 + (j & 1))) : "memory");
+      const int partner_bar = 3 + ((g * 2 + (h ^ 1)) * 2 + (j & 1));
+      float m_row;
+      if (!p.spec) {  // A/B knob (DMHA_SPEC=0): exchange first, then exponentials
+        asm volatile("bar.sync %0, 256;" ::"r"(partner_bar) : "memory");
+        m_row = fmaxf(m_loc, red_t[(h ^ 1) * kBM + r]);
+      } else {
+        m_row = m_loc;
       }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      const float m_use = (m_row == -INFINITY) ? 0.f : m_row;
       if constexpr (kSepP) {
         // exponentials first, then wait for PV_g(j-1) to have read P_g(j-1)
         if (kEmu == 0 || masked)
           sm::exp_inplace64<0>(s, sl2, m_use);
         else
           sm::exp_inplace64<(kEmu > 4 ? 4 : kEmu)>(s, sl2, m_use);
-        if (j > 0) {
-          ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
-          ptx::tc_fence_after();
-        }
-        l_run += sm::store_p64(s, tP);
       } else {
-        l_run += sm::exp_half(s, sl2, m_use, tP);
+        sm::exp_inplace64<0>(s, sl2, m_use);
       }
+      if (p.spec) {
+        asm volatile("bar.sync %0, 256;" ::"r"(partner_bar) : "memory");
+        m_row = fmaxf(m_loc, red_t[(h ^ 1) * kBM + r]);
+        if (__any_sync(0xffffffffu, m_row > m_loc)) {  // the partner half raised the max
+          const float f = m_row > m_loc ? ptx::ex2_approx(m_loc - m_row) : 1.f;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) s[c] *= f;
+        }
+      }
+      const bool warp_rescale = __any_sync(0xffffffffu, m_row != m_run);  // same in both halves
+      float alpha = 1.f;
+      if (warp_rescale) {
+        alpha = (m_row == m_run) ? 1.f : ptx::ex2_approx(m_run - m_row);
+        l_run *= alpha;
+        m_run = m_row;
+      }
+      if (kSepP && j > 0) {  // PV_g(j-1) has read P_g(j-1) (and finished O_g)
+        ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
+        ptx::tc_fence_after();
+      }
+      l_run += sm::store_p64(s, tP);
       if (warp_rescale && j > 0) {  // this half's D/2 columns of O
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -686,15 +712,72 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
-      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+      // Speculative max (kSpec, the one-warpgroup-per-tile schedule without
+      // separate P): once every row of the warp has a finite running max, the
+      // exponentials start at once with that stale max while the tile's row
+      // max is reduced alongside them (ALU pipe), so the max is off the
+      // softmax -> MMA chain.  If the tile max exceeds the running max by more
+      // than the threshold (rare after the first tile), the warp recomputes P
+      // with the new max — the same values the max-first order produces.
+      constexpr bool kSpec = !kSepP && kEmu == 0;
+      if (kSpec && p.spec && __all_sync(0xffffffffu, m_run != -INFINITY)) {
+        auto exp_store = [&](float m_use) {
+          float sum0 = 0.f, sum1 = 0.f;
+          float mx[8];
 #pragma unroll
-      for (int c = 4; c < 128; c += 4) {
-        mx0 = fmaxf(mx0, s[c]);
-        mx1 = fmaxf(mx1, s[c + 1]);
-        mx2 = fmaxf(mx2, s[c + 2]);
-        mx3 = fmaxf(mx3, s[c + 3]);
+          for (int i = 0; i < 8; ++i) mx[i] = s[i];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], sl2, -m_use));
+              const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], sl2, -m_use));
+              sum0 += e0;
+              sum1 += e1;
+              __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
+              pk[e] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            ptx::tmem_st16(tS + c * 16, pk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)  // this chunk's share of the row max
+              mx[i] = sm::fmax3(mx[i], fmaxf(s[32 * c + i], s[32 * c + 8 + i]),
+                                fmaxf(s[32 * c + 16 + i], s[32 * c + 24 + i]));
+          }
+          const float m8 = fmaxf(fmaxf(sm::fmax3(mx[0], mx[1], mx[2]), sm::fmax3(mx[3], mx[4], mx[5])),
+                                 fmaxf(mx[6], mx[7]));
+          return make_float2(sum0 + sum1, m8 * sl2);
+        };
+        float2 r = exp_store(m_run);
+        const bool warp_rescale = __any_sync(0xffffffffu, r.y > m_run + kRescaleThreshold);
+        float alpha = 1.f;
+        if (warp_rescale) {  // rare: redo P with the new max, rescale l and O
+          const float m_new = fmaxf(m_run, r.y);
+          alpha = ptx::ex2_approx(m_run - m_new);
+          l_run *= alpha;
+          m_run = m_new;
+          ptx::tmem_wait_st();
+          r = exp_store(m_run);
+        }
+        l_run += r.x;
+        if (warp_rescale && j > 0) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            float o[32];
+            ptx::tmem_ld32(tO + c * 32, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= alpha;
+            ptx::tmem_st32(tO + c * 32, o);
+          }
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
+        ptx::mbar_arrive(&p_ready[g]);
+        continue;
       }
-      const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const float mt = sm::row_max128(s) * sl2;
       const bool need = mt > m_run + kRescaleThreshold;
       const bool warp_rescale = __any_sync(0xffffffffu, need);
       float alpha = 1.f;
@@ -899,6 +982,8 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.kv_split = a.kv_split == 2 ? 2 : 1;
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.lse_bias = a.lse_bias;
+  p.spec = 1;
+  if (const char* e = std::getenv("DMHA_SPEC")) p.spec = std::atoi(e) != 0;
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H, p.kv_split);
   attn_fwd_sm100_kernel<D, E, S, I, PS><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);

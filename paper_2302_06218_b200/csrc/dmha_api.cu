@@ -1187,9 +1187,10 @@ int run_gemm(const void* A, const void* B, void* C, int64_t M, int N, int K) {
 int dmha_linear(const void* x, const void* w, void* y, int64_t M, int N, int K) {
   if (int rc = check_state()) return rc;
   if (g.dtype != DMHA_BF16) return fail(DMHA_ERR_UNSUPPORTED, "dmha_linear: bf16 only");
-  if (!x || !w || !y) return fail(DMHA_ERR_INVALID, "dmha_linear: null pointer");
   if (M < 0 || N < 1 || K < 1 || N % 8 != 0 || K % 8 != 0 || M > INT32_MAX)
     return fail(DMHA_ERR_INVALID, "dmha_linear: need M >= 0, N and K positive multiples of 8");
+  if (M == 0) return DMHA_OK;  // nothing to compute (x and y may be empty / null)
+  if (!x || !w || !y) return fail(DMHA_ERR_INVALID, "dmha_linear: null pointer");
   const void* ptrs[3] = {x, w, y};
   for (const void* p : ptrs)
     if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
