@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdmha.so"
 OBJ = PKG / "build"
-SOURCES = ["attn_fwd_sm100.cu", "attn_fwd_tf32.cu", "attn_fwd_fp32.cu", "lse_combine.cu", "headpar.cu", "selector.cu", "gemm_sm100.cu", "dmha_api.cu"]
+SOURCES = ["attn_fwd_sm100.cu", "attn_fwd_tf32.cu", "attn_fwd_fp32.cu", "lse_combine.cu", "headpar.cu", "selector.cu", "gemm_sm100.cu", "peer_link.cu", "dmha_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

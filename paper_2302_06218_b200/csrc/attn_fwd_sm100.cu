@@ -107,7 +107,8 @@ struct Params {
   int kv_split;    // 1, or 2: blockIdx.z picks one half of each CTA's key tiles
   int n_mblk;
   float lse_bias;  // fault injection (DMHA_FAULT=perturb_lse): added to lse_s in the combine; 0
-  int spec;        // speculative max on the one-warpgroup-per-tile path (DMHA_SPEC, default 1)
+  int spec;        // D = 64 split softmax: exchange the half-row maxima after the exponentials (DMHA_SPEC)
+  int alt;         // D = 128: the two softmax warpgroups take turns on MUFU (DMHA_ALT)
   unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
 
@@ -694,6 +695,85 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       ptx::mbar_wait(&s_full[g], static_cast<uint32_t>(j & 1));
       if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g, j);
       ptx::tc_fence_after();
+      // D = 128 default (one warpgroup per tile, P over S, MUFU only): the
+      // row is read from TMEM twice in 64-column halves — a max pass, then an
+      // exponential pass that packs P to bf16 and stores it over the first 64
+      // columns of S as it goes — so only 64 scores are live per thread and
+      // the exponentials run in place, back to back on MUFU (a whole row in
+      // registers made ptxas spill the MUFU results; ncu/SASS).
+      //
+      // Turn-taking (p.alt): the two softmax warpgroups run their
+      // exponential passes one after the other — WG1 starts tile j when WG0
+      // has finished it, WG0 starts tile j+1 when WG1 has finished tile j — so
+      // each has MUFU to itself, and a warpgroup's max pass overlaps the
+      // other's exponentials (named barriers 1 = "WG0 may go", 2 = "WG1 may
+      // go"; 128 arrive + 128 sync each).
+      constexpr bool kTwoPass = !kSepP && kEmu == 0;
+      const bool alt = !kSepP && p.alt;
+      auto turn_wait = [&]() {
+        if (alt && (g == 1 || j > 0)) asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+      };
+      auto turn_done = [&]() {
+        if (alt) asm volatile("bar.arrive %0, 256;" ::"r"(2 - g) : "memory");
+      };
+      if constexpr (kTwoPass) {
+        const int64_t nvq = klim - static_cast<int64_t>(jt0 + j) * kBN;
+        const int nval = nvq < 0 ? 0 : (nvq > kBN ? kBN : static_cast<int>(nvq));
+        const bool msk = !__all_sync(0xffffffffu, nval >= kBN);
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float t[64];
+          sm::load64(tS + 64 * hh, t);
+          if (msk) sm::mask64(t, nval - 64 * hh);
+          sm::max64_into(mx, t);
+        }
+        const float mt = fmaxf(fmaxf(sm::fmax3(mx[0], mx[1], mx[2]), sm::fmax3(mx[3], mx[4], mx[5])),
+                               fmaxf(mx[6], mx[7])) * sl2;
+        const bool warp_rescale = __any_sync(0xffffffffu, mt > m_run + kRescaleThreshold);
+        float alpha = 1.f;
+        if (warp_rescale) {
+          const float m_new = fmaxf(m_run, mt);
+          alpha = (m_new == -INFINITY) ? 1.f : ptx::ex2_approx(m_run - m_new);
+          l_run *= alpha;
+          m_run = m_new;
+        }
+        const bool tr = threadIdx.x % 128 == 0;  // timeline stamps (trace_x, CTA 0)
+        if (tr) trace_x(p, 9 * g + 0, j);
+        turn_wait();
+        if (tr) trace_x(p, 9 * g + 1, j);
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float t[64];
+          sm::load64(tS + 64 * hh, t);
+          if (msk) sm::mask64(t, nval - 64 * hh);
+          sm::exp_pack_store64(t, sl2, m_use, tS + 32 * hh, acc);
+        }
+        if (tr) trace_x(p, 9 * g + 2, j);
+        turn_done();
+        l_run += (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
+        if (warp_rescale && j > 0) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            float o[32];
+            ptx::tmem_ld32(tO + c * 32, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= alpha;
+            ptx::tmem_st32(tO + c * 32, o);
+          }
+        }
+        ptx::tmem_wait_st();
+        if (tr) trace_x(p, 9 * g + 3, j);
+        ptx::tc_fence_before();
+        if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
+        ptx::mbar_arrive(&p_ready[g]);
+        continue;
+      }
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -712,71 +792,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
-      // Speculative max (kSpec, the one-warpgroup-per-tile schedule without
-      // separate P): once every row of the warp has a finite running max, the
-      // exponentials start at once with that stale max while the tile's row
-      // max is reduced alongside them (ALU pipe), so the max is off the
-      // softmax -> MMA chain.  If the tile max exceeds the running max by more
-      // than the threshold (rare after the first tile), the warp recomputes P
-      // with the new max — the same values the max-first order produces.
-      constexpr bool kSpec = !kSepP && kEmu == 0;
-      if (kSpec && p.spec && __all_sync(0xffffffffu, m_run != -INFINITY)) {
-        auto exp_store = [&](float m_use) {
-          float sum0 = 0.f, sum1 = 0.f;
-          float mx[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) mx[i] = s[i];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], sl2, -m_use));
-              const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], sl2, -m_use));
-              sum0 += e0;
-              sum1 += e1;
-              __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
-              pk[e] = *reinterpret_cast<uint32_t*>(&b);
-            }
-            ptx::tmem_st16(tS + c * 16, pk);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)  // this chunk's share of the row max
-              mx[i] = sm::fmax3(mx[i], fmaxf(s[32 * c + i], s[32 * c + 8 + i]),
-                                fmaxf(s[32 * c + 16 + i], s[32 * c + 24 + i]));
-          }
-          const float m8 = fmaxf(fmaxf(sm::fmax3(mx[0], mx[1], mx[2]), sm::fmax3(mx[3], mx[4], mx[5])),
-                                 fmaxf(mx[6], mx[7]));
-          return make_float2(sum0 + sum1, m8 * sl2);
-        };
-        float2 r = exp_store(m_run);
-        const bool warp_rescale = __any_sync(0xffffffffu, r.y > m_run + kRescaleThreshold);
-        float alpha = 1.f;
-        if (warp_rescale) {  // rare: redo P with the new max, rescale l and O
-          const float m_new = fmaxf(m_run, r.y);
-          alpha = ptx::ex2_approx(m_run - m_new);
-          l_run *= alpha;
-          m_run = m_new;
-          ptx::tmem_wait_st();
-          r = exp_store(m_run);
-        }
-        l_run += r.x;
-        if (warp_rescale && j > 0) {
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            float o[32];
-            ptx::tmem_ld32(tO + c * 32, o);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= alpha;
-            ptx::tmem_st32(tO + c * 32, o);
-          }
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
-        ptx::mbar_arrive(&p_ready[g]);
-        continue;
-      }
+      turn_wait();
       const float mt = sm::row_max128(s) * sl2;
       const bool need = mt > m_run + kRescaleThreshold;
       const bool warp_rescale = __any_sync(0xffffffffu, need);
@@ -835,6 +851,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       } else {
         l_run += sm::exp_tile<kEmu>(s, sl2, m_use, tP);
       }
+      turn_done();
       // O_g holds PV_g(j-1) (complete: covered by the S_g(j) commit, or by the
       // pv_done wait when D = 64) and PV_g(j) is not issued before p_ready, so
       // O can be rescaled in place here.
@@ -854,6 +871,8 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
       ptx::mbar_arrive(&p_ready[g]);
     }
+    // WG0 consumes WG1's hand-over of the last tile (no dangling arrival)
+    if (!kSepP && p.alt && g == 0 && nkv > 0) asm volatile("bar.sync 1, 256;" ::: "memory");
     if (nkv > 0) {
       ptx::mbar_wait(&o_final[g], 0);
       ptx::tc_fence_after();
@@ -982,8 +1001,10 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.kv_split = a.kv_split == 2 ? 2 : 1;
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.lse_bias = a.lse_bias;
-  p.spec = 1;
+  p.spec = 0;  // measured slower on the D = 64 split softmax
   if (const char* e = std::getenv("DMHA_SPEC")) p.spec = std::atoi(e) != 0;
+  p.alt = 1;
+  if (const char* e = std::getenv("DMHA_ALT")) p.alt = std::atoi(e) != 0;
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H, p.kv_split);
   attn_fwd_sm100_kernel<D, E, S, I, PS><<<grid, Roles<S>::kThreads, C::kSmemBytes, stream>>>(tq, tk, tv, p);

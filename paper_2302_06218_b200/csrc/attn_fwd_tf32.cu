@@ -29,6 +29,12 @@
 #include "kernels.h"
 #include "ptx_sm100.cuh"
 
+// TF32_WAIT: the kernel's mbarrier wait (tools/tf32_kernel_probe.cu
+// redefines it as a bounded wait that reports where a CTA stalls).
+#ifndef TF32_WAIT
+#define TF32_WAIT(bar, phase, tag) ptx::mbar_wait(bar, phase)
+#endif
+
 namespace dmha {
 namespace {
 
@@ -181,15 +187,20 @@ __global__ void __launch_bounds__(128, 1)
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
-    if (tid == 0) {
-      ptx::tc_fence_after();
-      const uint32_t d = tmem + C::kTmemS;
-      mma_tf32_kloop(d, sbase + C::kQl, kBM, sbase + C::kKh, kBN, D, C::kIdescS, false);
-      mma_tf32_kloop(d, sbase + C::kQh, kBM, sbase + C::kKl, kBN, D, C::kIdescS, true);
-      mma_tf32_kloop(d, sbase + C::kQh, kBM, sbase + C::kKh, kBN, D, C::kIdescS, true);
-      ptx::mma_commit(bar);
+    // one thread issues; the rest of its warp waits at __syncwarp (not in the
+    // mbarrier spin below, which could starve the issuing lane)
+    if (tid < 32) {
+      if (tid == 0) {
+        ptx::tc_fence_after();
+        const uint32_t d = tmem + C::kTmemS;
+        mma_tf32_kloop(d, sbase + C::kQl, kBM, sbase + C::kKh, kBN, D, C::kIdescS, false);
+        mma_tf32_kloop(d, sbase + C::kQh, kBM, sbase + C::kKl, kBN, D, C::kIdescS, true);
+        mma_tf32_kloop(d, sbase + C::kQh, kBM, sbase + C::kKh, kBN, D, C::kIdescS, true);
+        ptx::mma_commit(bar);
+      }
+      __syncwarp();
     }
-    ptx::mbar_wait(bar, phase);
+    TF32_WAIT(bar, phase, 1000 + jt);
     phase ^= 1;
     ptx::tc_fence_after();
     // ---- online softmax of this row (fp32, exp2 domain)
@@ -238,15 +249,18 @@ __global__ void __launch_bounds__(128, 1)
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
-    if (tid == 0) {
-      ptx::tc_fence_after();
-      const uint32_t d = tmem + C::kTmemO;
-      mma_tf32_kloop(d, sbase + C::kPl, kBM, sbase + C::kVh, D, kBN, C::kIdescO, jt > 0);
-      mma_tf32_kloop(d, sbase + C::kPh, kBM, sbase + C::kVl, D, kBN, C::kIdescO, true);
-      mma_tf32_kloop(d, sbase + C::kPh, kBM, sbase + C::kVh, D, kBN, C::kIdescO, true);
-      ptx::mma_commit(bar);
+    if (tid < 32) {
+      if (tid == 0) {
+        ptx::tc_fence_after();
+        const uint32_t d = tmem + C::kTmemO;
+        mma_tf32_kloop(d, sbase + C::kPl, kBM, sbase + C::kVh, D, kBN, C::kIdescO, jt > 0);
+        mma_tf32_kloop(d, sbase + C::kPh, kBM, sbase + C::kVl, D, kBN, C::kIdescO, true);
+        mma_tf32_kloop(d, sbase + C::kPh, kBM, sbase + C::kVh, D, kBN, C::kIdescO, true);
+        ptx::mma_commit(bar);
+      }
+      __syncwarp();
     }
-    ptx::mbar_wait(bar, phase);  // PV done: K/V/P buffers free, O complete
+    TF32_WAIT(bar, phase, 2000 + jt);  // PV done: K/V/P buffers free, O complete
     phase ^= 1;
     ptx::tc_fence_after();
   }

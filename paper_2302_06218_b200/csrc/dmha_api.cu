@@ -29,6 +29,7 @@
 
 #include "../../include/dmha.h"
 #include "kernels.h"
+#include "peer_link.h"
 
 namespace {
 
@@ -66,6 +67,13 @@ struct State {
   cudaStream_t stream = nullptr;  // compute stream (user's)
   cudaStream_t comm = nullptr;    // NCCL stream (library-owned, high priority)
   ncclComm_t nccl = nullptr;
+  // K/V transport of the ring at world size > 1 (DMHA_TRANSPORT at init):
+  // 0 = NCCL send/recv (default), 1 = copy-engine pulls from peer memory
+  // (CUDA IPC, NEXT-2).  With the peer transport the NCCL communicator is
+  // created lazily, only for the entry points that need a collective.
+  int transport = 0;
+  dmha::PeerLink* peer = nullptr;
+  unsigned char uid[128] = {};
   cudaEvent_t ev_start = nullptr, ev_recv[2] = {nullptr, nullptr},
               ev_done[2] = {nullptr, nullptr}, ev_comm_end = nullptr;
   // host path pipelining (dmha_forward_host at world size 1)
@@ -182,7 +190,7 @@ void update_ws_stat() {
   g.stats.workspace_bytes = 2 * g.kv_bytes + (g.acc_elems + g.part_elems) * 4 +
                             (g.lse_elems + g.part_lse_elems) * 4 +
                             g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes + g.mha_bytes +
-                            g.sel_bytes;
+                            g.sel_bytes + (g.peer ? dmha::peer_pub_bytes(g.peer) : 0);
 }
 
 int alloc_or_oom(void** p, size_t bytes, const char* what) {
@@ -224,7 +232,9 @@ size_t ring_ws_bytes(int P, int64_t Lloc, int D, int H) {
   const size_t lse = static_cast<size_t>(Lloc) * H;
   if (P == 1) return split_kv_active(Lloc, D, H) ? 2 * (elems * 4 + lse * 4) : 0;
   const size_t parts = fused_combine(D) ? 1 : 2;
-  return 2 * (2 * elems * elem_bytes(g.dtype)) + parts * (elems * 4 + lse * 4);
+  // + the published K/V block of the peer transport (NEXT-2)
+  const size_t pub = g.transport == 1 ? 2 * elems * elem_bytes(g.dtype) : 0;
+  return 2 * (2 * elems * elem_bytes(g.dtype)) + parts * (elems * 4 + lse * 4) + pub;
 }
 
 // Ring accumulators (always), the partial buffers (unfused combine only) and
@@ -454,6 +464,16 @@ int ring_compute_step(int s, int P, int r, int layout, const void* q, const void
   }
 }
 
+// The NCCL communicator (created at init with the NCCL transport, on first
+// use with the peer transport).  Collective: every rank reaches it together.
+int need_nccl() {
+  if (g.world == 1 || g.nccl) return DMHA_OK;
+  ncclUniqueId id;
+  memcpy(&id, g.uid, sizeof(id));
+  CK_NCCL(ncclCommInitRank(&g.nccl, g.world, id, g.rank));
+  return DMHA_OK;
+}
+
 int poll_nccl() {
   if (!g.nccl) return DMHA_OK;
   ncclResult_t st = ncclSuccess;
@@ -512,6 +532,22 @@ struct CopyTransport final : Transport {
     CK_CUDA(cudaMemcpyAsync(dst, k_all + src_next * shard, blk, cudaMemcpyDeviceToDevice, g.comm));
     CK_CUDA(cudaMemcpyAsync(dst + blk, v_all + src_next * shard, blk, cudaMemcpyDeviceToDevice,
                             g.comm));
+    return DMHA_OK;
+  }
+};
+
+// NEXT-2 peer transport: the block of ring step s+1 is rank src_next's own
+// K/V, which that rank published in its IPC-shared buffer at the start of the
+// forward (see peer_forward); pull it with the copy engine once its
+// "published" event has fired.  No relay: each block crosses the link once.
+struct PeerTransport final : Transport {
+  int P, r;
+  PeerTransport(int P_, int r_) : P(P_), r(r_) {}
+  int exchange(const dmha_ring_plan&, int s, const void*, const void*, char* dst,
+               size_t blk) override {
+    const int src_next = ((r - s - 1) % P + P) % P;
+    CK_CUDA(cudaStreamWaitEvent(g.comm, dmha::peer_pub_event(g.peer, src_next), 0));
+    CK_CUDA(cudaMemcpyAsync(dst, dmha::peer_pub(g.peer, src_next), 2 * blk, cudaMemcpyDefault, g.comm));
     return DMHA_OK;
   }
 };
@@ -589,7 +625,8 @@ int ring_forward(int P, int r, int layout, const void* q, const void* k, const v
 // deadlock or corrupt the exchange).
 int check_collective_contract(int64_t L, int D, int H, int causal) {
   const char* e = std::getenv("DMHA_CHECK_COLLECTIVE");
-  if (!e || std::atoi(e) == 0 || g.world == 1 || !g.nccl) return DMHA_OK;
+  if (!e || std::atoi(e) == 0 || g.world == 1) return DMHA_OK;
+  if (int rc = need_nccl()) return rc;
   int64_t h[8] = {L, D, H, causal ? 1 : 0, -L, -D, -H, causal ? -1 : 0};
   int64_t* d = nullptr;
   CK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), g.stream));
@@ -765,10 +802,20 @@ int dmha_init(int world_size, int rank, const void* unique_id, int device, int d
     CK_CUDA(cudaEventCreateWithFlags(&g.ev_recv[i], cudaEventDisableTiming));
     CK_CUDA(cudaEventCreateWithFlags(&g.ev_done[i], cudaEventDisableTiming));
   }
+  if (const char* e = std::getenv("DMHA_TRANSPORT")) {
+    if (!strcmp(e, "peer")) g.transport = 1;
+    else if (strcmp(e, "nccl") != 0)
+      return fail(DMHA_ERR_INVALID, "dmha_init: DMHA_TRANSPORT must be nccl or peer, got %s", e);
+  }
   if (world_size > 1) {
-    ncclUniqueId id;
-    memcpy(&id, unique_id, sizeof(id));
-    CK_NCCL(ncclCommInitRank(&g.nccl, world_size, id, rank));
+    memcpy(g.uid, unique_id, sizeof(g.uid));
+    if (g.transport == 1) {
+      std::string err;
+      if (int rc = dmha::peer_open(&g.peer, unique_id, world_size, rank, device, &err))
+        return fail(rc, "%s", err.c_str());
+    } else if (int rc = need_nccl()) {
+      return rc;
+    }
   }
   g.inited = true;
   g_last_error.clear();
@@ -800,6 +847,7 @@ int dmha_finalize(void) {
   for (cudaEvent_t e : g.pool) cudaEventDestroy(e);
   g.pool.clear();
   if (g.nccl) ncclCommDestroy(g.nccl);
+  if (g.peer) dmha::peer_close(g.peer);
   cudaEvent_t evs[6] = {g.ev_start, g.ev_comm_end, g.ev_recv[0], g.ev_recv[1], g.ev_done[0],
                         g.ev_done[1]};
   for (cudaEvent_t e : evs)
@@ -872,6 +920,35 @@ int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_
   return DMHA_OK;
 }
 
+// One rank's forward with the peer transport (NEXT-2):
+//   host barrier B1            every rank has issued its previous forward's
+//                              "done pulling" record
+//   stream waits done(peers)   nobody still reads my published buffer
+//   copy k, v -> published buffer; record "published" on the stream
+//   host barrier B2            every "published" record precedes the pulls
+//   ring_forward(PeerTransport): step s+1's block pulled from its owner
+//   record "done pulling" on the comm stream
+int peer_forward(const void* q, const void* k, const void* v, void* out, float* lse, int64_t L,
+                 int D, int H, int causal) {
+  const int P = g.world, r = g.rank;
+  const size_t blk = static_cast<size_t>(L / P) * H * D * elem_bytes(g.dtype);
+  std::string err;
+  if (int rc = dmha::peer_ensure_pub(g.peer, 2 * blk, &err)) return fail(rc, "%s", err.c_str());
+  update_ws_stat();
+  if (int rc = dmha::peer_barrier(g.peer, &err)) return fail(rc, "%s", err.c_str());
+  for (int p = 0; p < P; ++p)
+    if (p != r) CK_CUDA(cudaStreamWaitEvent(g.stream, dmha::peer_done_event(g.peer, p), 0));
+  char* pub = static_cast<char*>(dmha::peer_local_pub(g.peer));
+  CK_CUDA(cudaMemcpyAsync(pub, k, blk, cudaMemcpyDeviceToDevice, g.stream));
+  CK_CUDA(cudaMemcpyAsync(pub + blk, v, blk, cudaMemcpyDeviceToDevice, g.stream));
+  CK_CUDA(cudaEventRecord(dmha::peer_pub_event(g.peer, r), g.stream));
+  if (int rc = dmha::peer_barrier(g.peer, &err)) return fail(rc, "%s", err.c_str());
+  PeerTransport tx(P, r);
+  if (int rc = ring_forward(P, r, g.layout, q, k, v, out, lse, L, D, H, causal, tx)) return rc;
+  CK_CUDA(cudaEventRecord(dmha::peer_done_event(g.peer, r), g.comm));
+  return DMHA_OK;
+}
+
 int dmha_forward(const void* q, const void* k, const void* v, void* out, float* lse, int64_t L,
                  int D, int H, int causal) {
   if (int rc = check_state()) return rc;
@@ -879,9 +956,13 @@ int dmha_forward(const void* q, const void* k, const void* v, void* out, float* 
   if (int rc = poll_nccl()) return rc;
   if (int rc = check_collective_contract(L, D, H, causal)) return rc;
   begin_forward();
-  NcclTransport tx;
-  if (int rc = ring_forward(g.world, g.rank, g.layout, q, k, v, out, lse, L, D, H, causal ? 1 : 0, tx))
-    return rc;
+  if (g.world > 1 && g.transport == 1) {
+    if (int rc = peer_forward(q, k, v, out, lse, L, D, H, causal ? 1 : 0)) return rc;
+  } else {
+    NcclTransport tx;
+    if (int rc = ring_forward(g.world, g.rank, g.layout, q, k, v, out, lse, L, D, H, causal ? 1 : 0, tx))
+      return rc;
+  }
   g.stats.forwards++;
   return DMHA_OK;
 }
@@ -1057,6 +1138,7 @@ int dmha_forward_headpar(const void* q, const void* k, const void* v, void* out,
   const int P = g.world, r = g.rank;
   causal = causal ? 1 : 0;
   if (P == 1) return dmha_forward(q, k, v, out, lse, L, D, H, causal);
+  if (int rc = need_nccl()) return rc;
   if (int rc = check_collective_contract(L, D, H, causal)) return rc;
   begin_forward();
   const int64_t Lloc = L / P;
@@ -1309,6 +1391,7 @@ int dmha_select(const void* x, int64_t n_rows, int width, int scorer, const void
   CK_LAUNCH(dmha::launch_selector_scan(counts, n_rows, offsets, slots, g.stream));
   g.stats.kernel_launches += 2;
   if (g.world > 1) {
+    if (int rc = need_nccl()) return rc;
     CK_NCCL(ncclAllReduce(slots, slots + 1, 1, ncclInt64, ncclSum, g.nccl, g.stream));
   } else {
     CK_CUDA(cudaMemcpyAsync(slots + 1, slots, 8, cudaMemcpyDeviceToDevice, g.stream));

@@ -40,7 +40,16 @@ dmha.finalize()
 #  0 before K_j wait, 1 K_j landed, 2 s_free seen, 3 V_{j-1} landed, 4 PV_{j-1} committed;
 #  producer: 5/14 before kv_empty wait for K_j / V_j, 6/15 slot free
 x = buf.view(-1)[18 * 64: 36 * 64].view(18, 64).cpu().numpy().astype(np.int64)
-if x[0][10]:
+if D == 128 and x[0][10]:
+    # in-place D = 128 softmax sub-phases per WG g (base 9g): 0 max done, 1 turn
+    # granted, 2 exps done, 3 P stored; relative to that WG's "saw S" (t[0][2g])
+    for g in range(2):
+        js = range(8, 60)
+        saw = t[0][2 * g]
+        ph = [np.mean([x[9 * g + e][j] - (saw[j] if e == 0 else x[9 * g + e - 1][j]) for j in js]) for e in range(4)]
+        pr = np.mean([t[0][2 * g + 1][j] - x[9 * g + 3][j] for j in js])
+        print(f"  WG{g}: load+max {ph[0]:.0f}  turn-wait {ph[1]:.0f}  exps {ph[2]:.0f}  pack+store {ph[3]:.0f}  ->P-ready {pr:.0f}")
+elif x[0][10]:
     x0 = t[0][0][0]
     names = ["g0 preK", "g0 Kland", "g0 sfree", "g0 Vland", "g0 PVdone", "prodK pre", "prodK free", "", "",
              "g1 preK", "g1 Kland", "g1 sfree", "g1 Vland", "g1 PVdone", "prodV pre", "prodV free", "", ""]
