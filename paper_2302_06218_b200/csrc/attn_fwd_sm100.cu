@@ -695,20 +695,11 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       ptx::mbar_wait(&s_full[g], static_cast<uint32_t>(j & 1));
       if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g, j);
       ptx::tc_fence_after();
-      // D = 128 default (one warpgroup per tile, P over S, MUFU only): the
-      // row is read from TMEM twice in 64-column halves — a max pass, then an
-      // exponential pass that packs P to bf16 and stores it over the first 64
-      // columns of S as it goes — so only 64 scores are live per thread and
-      // the exponentials run in place, back to back on MUFU (a whole row in
-      // registers made ptxas spill the MUFU results; ncu/SASS).
-      //
-      // Turn-taking (p.alt): the two softmax warpgroups run their
-      // exponential passes one after the other — WG1 starts tile j when WG0
-      // has finished it, WG0 starts tile j+1 when WG1 has finished tile j — so
-      // each has MUFU to itself, and a warpgroup's max pass overlaps the
-      // other's exponentials (named barriers 1 = "WG0 may go", 2 = "WG1 may
-      // go"; 128 arrive + 128 sync each).
-      constexpr bool kTwoPass = !kSepP && kEmu == 0;
+      // Turn-taking (p.alt, DMHA_ALT=1): the two softmax warpgroups run their
+      // exponentials one after the other — WG1 starts tile j when WG0 has
+      // finished it, WG0 starts tile j+1 when WG1 has finished tile j (named
+      // barriers 1 = "WG0 may go", 2 = "WG1 may go"; 128 arrive + 128 sync).
+      // Measured within noise of the free-running default.
       const bool alt = !kSepP && p.alt;
       auto turn_wait = [&]() {
         if (alt && (g == 1 || j > 0)) asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
@@ -716,64 +707,6 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       auto turn_done = [&]() {
         if (alt) asm volatile("bar.arrive %0, 256;" ::"r"(2 - g) : "memory");
       };
-      if constexpr (kTwoPass) {
-        const int64_t nvq = klim - static_cast<int64_t>(jt0 + j) * kBN;
-        const int nval = nvq < 0 ? 0 : (nvq > kBN ? kBN : static_cast<int>(nvq));
-        const bool msk = !__all_sync(0xffffffffu, nval >= kBN);
-        float mx[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float t[64];
-          sm::load64(tS + 64 * hh, t);
-          if (msk) sm::mask64(t, nval - 64 * hh);
-          sm::max64_into(mx, t);
-        }
-        const float mt = fmaxf(fmaxf(sm::fmax3(mx[0], mx[1], mx[2]), sm::fmax3(mx[3], mx[4], mx[5])),
-                               fmaxf(mx[6], mx[7])) * sl2;
-        const bool warp_rescale = __any_sync(0xffffffffu, mt > m_run + kRescaleThreshold);
-        float alpha = 1.f;
-        if (warp_rescale) {
-          const float m_new = fmaxf(m_run, mt);
-          alpha = (m_new == -INFINITY) ? 1.f : ptx::ex2_approx(m_run - m_new);
-          l_run *= alpha;
-          m_run = m_new;
-        }
-        const bool tr = threadIdx.x % 128 == 0;  // timeline stamps (trace_x, CTA 0)
-        if (tr) trace_x(p, 9 * g + 0, j);
-        turn_wait();
-        if (tr) trace_x(p, 9 * g + 1, j);
-        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float t[64];
-          sm::load64(tS + 64 * hh, t);
-          if (msk) sm::mask64(t, nval - 64 * hh);
-          sm::exp_pack_store64(t, sl2, m_use, tS + 32 * hh, acc);
-        }
-        if (tr) trace_x(p, 9 * g + 2, j);
-        turn_done();
-        l_run += (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
-        if (warp_rescale && j > 0) {
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            float o[32];
-            ptx::tmem_ld32(tO + c * 32, o);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= alpha;
-            ptx::tmem_st32(tO + c * 32, o);
-          }
-        }
-        ptx::tmem_wait_st();
-        if (tr) trace_x(p, 9 * g + 3, j);
-        ptx::tc_fence_before();
-        if (threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
-        ptx::mbar_arrive(&p_ready[g]);
-        continue;
-      }
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -1003,7 +936,7 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.lse_bias = a.lse_bias;
   p.spec = 0;  // measured slower on the D = 64 split softmax
   if (const char* e = std::getenv("DMHA_SPEC")) p.spec = std::atoi(e) != 0;
-  p.alt = 1;
+  p.alt = 0;
   if (const char* e = std::getenv("DMHA_ALT")) p.alt = std::atoi(e) != 0;
   p.trace = g_trace;
   dim3 grid(p.n_mblk, a.H, p.kv_split);

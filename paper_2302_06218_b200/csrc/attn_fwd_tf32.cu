@@ -233,7 +233,10 @@ __global__ void __launch_bounds__(128, 1)
       *reinterpret_cast<float4*>(sm + C::kPl + sw_off(kBM, tid, c >> 2)) = lo;
     }
     l_run = l_run * alpha + sum;
-    if (jt > 0 && m_new > m_run) {  // O (complete: the previous PV was waited for) *= alpha
+    // O (complete: the previous PV was waited for) *= alpha.  tcgen05.ld/st are
+    // warp-collective (.sync.aligned): the whole warp takes the branch when any
+    // of its rows needs it (alpha = 1 for the others).
+    if (__any_sync(0xffffffffu, jt > 0 && m_new > m_run)) {
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         float o[32];

@@ -157,25 +157,6 @@ __device__ __forceinline__ void exp_inplace(float (&s)[128], float sl2, float m_
   }
 }
 
-// exp_inplace with the row's raw maximum reduced alongside (ALU pipe, read
-// before each pair is overwritten): s <- exp2(s*scale*log2e - m); returns
-// max_c s[c] (unscaled).
-__device__ __forceinline__ float exp_max_inplace(float (&s)[128], float sl2, float m_use) {
-  const float2 sc2 = make_float2(sl2, sl2);
-  const float2 nm2 = make_float2(-m_use, -m_use);
-  float mx[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < 64; ++i) {
-    mx[i & 7] = fmax3(mx[i & 7], s[2 * i], s[2 * i + 1]);
-    const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
-    s[2 * i] = ptx::ex2_approx(x.x);
-    s[2 * i + 1] = ptx::ex2_approx(x.y);
-  }
-  return fmaxf(fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5])), fmaxf(mx[6], mx[7]));
-}
-
 // Pass 2: pack the 128 exponentials to bf16, store them as 64 TMEM columns at
 // tP (16-column chunks) and return their fp32 sum.
 __device__ __forceinline__ float store_p(const float (&s)[128], uint32_t tP) {
@@ -195,52 +176,6 @@ __device__ __forceinline__ float store_p(const float (&s)[128], uint32_t tP) {
   }
   const float2 t = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
   return t.x + t.y;
-}
-
-// Two-pass-over-TMEM helpers (D = 128 default): the row is read from TMEM in
-// 64-column halves, once for the max and once for the exponentials, so only
-// 64 scores are live per thread (a whole 128-column row plus the exp outputs
-// does not fit the 168-register budget of a 12-warp CTA: ptxas spilled the
-// MUFU results inside the exponential loop).
-__device__ __forceinline__ void load64(uint32_t taddr, float (&t)[64]) {
-  ptx::tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(&t[0]));
-  ptx::tmem_ld32(taddr + 32, *reinterpret_cast<float(*)[32]>(&t[32]));
-  ptx::tmem_wait_ld();
-}
-__device__ __forceinline__ void mask64(float (&t)[64], int nvalid_here) {
-#pragma unroll
-  for (int c = 0; c < 64; ++c) t[c] = c < nvalid_here ? t[c] : -INFINITY;
-}
-__device__ __forceinline__ void max64_into(float (&mx)[8], const float (&t)[64]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    mx[i] = fmax3(fmax3(mx[i], t[i], t[8 + i]), fmax3(t[16 + i], t[24 + i], t[32 + i]),
-                  fmax3(t[40 + i], t[48 + i], t[56 + i]));
-}
-// t <- exp2(t*scale*log2e - m) in place, then pack to bf16, store the 32 P
-// columns at tP and accumulate the fp32 sum into acc.
-__device__ __forceinline__ void exp_pack_store64(float (&t)[64], float sl2, float m_use, uint32_t tP,
-                                                 float2 (&acc)[2]) {
-  const float2 sc2 = make_float2(sl2, sl2);
-  const float2 nm2 = make_float2(-m_use, -m_use);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const float2 x = __ffma2_rn(make_float2(t[2 * i], t[2 * i + 1]), sc2, nm2);
-    t[2 * i] = ptx::ex2_approx(x.x);
-    t[2 * i + 1] = ptx::ex2_approx(x.y);
-  }
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t pk[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float2 pe = make_float2(t[32 * c + 2 * e], t[32 * c + 2 * e + 1]);
-      acc[e & 1] = __fadd2_rn(acc[e & 1], pe);
-      __nv_bfloat162 b = __floats2bfloat162_rn(pe.x, pe.y);
-      pk[e] = *reinterpret_cast<uint32_t*>(&b);
-    }
-    ptx::tmem_st16(tP + c * 16, pk);
-  }
 }
 
 // Pass 2 for P in shared memory (D = 128, kPS): pack the 128 exponentials of
