@@ -282,11 +282,16 @@ def roofline_of(w, st, steps, world, step_ms_local, peaks, peak_src):
         except Exception:
             traffic = None
     if w["dtype"] == "fp32":
-        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-        return {"bound": "alu", "kernel": "attn_fwd_fp32", "achieved": achieved,
+        # 3xTF32 on tcgen05 kind::tf32 (attn_fwd_tf32.cu): tensor-bound at the
+        # TF32 rate = the measured bf16 peak x the nominal tf32/bf16 ratio
+        # (1.125 / 2.25 PF dense); algorithmic FLOP counted once, although
+        # each product takes three tensor passes
+        bf = float(peaks.get("bf16_tflops", 1590.0))
+        peak = bf * 0.5
+        return {"bound": "tensor", "kernel": "attn_fwd_tf32x3_kernel", "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_kind": f"FP32 FMA pipe, 148x128x2 FLOP/clk at {sm_mhz:.0f} MHz (derived)",
+                "peak_kind": f"TF32 dense = measured bf16 burst {bf:.0f} x 0.5 (nominal ratio), {peak_src}",
+                "frac_of_3pass_work": 3 * achieved / peak,
                 "flops_per_launch": flops_per_launch, "launch_ms": attn_ms_avg,
                 "share_of_step": attn_share}
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))

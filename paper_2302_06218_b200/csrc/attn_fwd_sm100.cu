@@ -62,6 +62,13 @@ struct Roles {
   static constexpr int kThreads = (kSm + 4) * 32;
 };
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
+#ifndef DMHA_SOFTMAX_REGS
+#define DMHA_SOFTMAX_REGS 0
+#endif
+constexpr int kSmRegs = DMHA_SOFTMAX_REGS;  // 0: no re-balancing
+constexpr int kOtherRegs = kSmRegs > 0 ? ((384 * 168 - 256 * kSmRegs) / 128) / 8 * 8 : 0;
+static_assert(kSmRegs == 0 || (kSmRegs % 8 == 0 && kSmRegs <= 256 && kOtherRegs >= 24),
+              "setmaxnreg budget");
 
 // kPS (D = 128 only): P_g(j) goes to shared memory instead of over S_g's TMEM
 // columns, so QK^T(j+1) can run during softmax(j) (the separate-P schedule of
@@ -233,6 +240,16 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Register re-balancing (one-warpgroup-per-tile schedule): the producer /
+  // MMA / idle warpgroup (warps 8-11, all four execute the dec) hands
+  // registers to the two softmax warpgroups, whose 128-score rows otherwise
+  // leave ptxas too few registers to keep several MUFU results in flight
+  // (ncu: short-scoreboard stalls on MUFU.EX2 with a reused destination).
+  // 384 threads x 168 = 256 x kSmRegs + 128 x kOtherRegs.
+  if constexpr (!kSplit && kSmRegs > 0) {
+    if (warp >= 8) ptx::setmaxnreg_dec<kOtherRegs>();
+    else ptx::setmaxnreg_inc<kSmRegs>();
+  }
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer

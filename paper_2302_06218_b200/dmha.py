@@ -11,11 +11,16 @@ call raises ``DmhaError``.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
 
 _LIB_PATH = Path(__file__).resolve().parent / "libdmha.so"
+# A/B tooling only: DMHA_LIB names another in-tree build of the same library
+# (e.g. paper_2302_06218_b200/build_ab/libdmha.so compiled with other flags).
+if os.environ.get("DMHA_LIB"):
+    _LIB_PATH = Path(os.environ["DMHA_LIB"]).resolve()
 
 OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_STATE = 0, -1, -2, -3, -4, -5, -6
 BF16, FP32 = 0, 1
