@@ -114,7 +114,6 @@ struct Params {
   int kv_split;    // 1, or 2: blockIdx.z picks one half of each CTA's key tiles
   int n_mblk;
   float lse_bias;  // fault injection (DMHA_FAULT=perturb_lse): added to lse_s in the combine; 0
-  int spec;        // D = 64 split softmax: exchange the half-row maxima after the exponentials (DMHA_SPEC)
   int alt;         // D = 128: the two softmax warpgroups take turns on MUFU (DMHA_ALT)
   unsigned long long* trace;  // debug timeline (dmha_debug_set_trace), usually null
 };
@@ -538,60 +537,35 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 64; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
-      // Row max without a barrier before the exponentials: each half takes
-      // m_loc = its own half's max when that exceeds the running max by more
-      // than the threshold (else the stale running max), publishes m_loc with
-      // a non-blocking bar.arrive, computes its exponentials, and only then
-      // reads the partner's m_loc (barrier (g, partner, tile parity), long
-      // satisfied by then).  Both halves end with the same row max
-      // m_row = max(m_loc, m_loc'); a half whose m_loc is below it scales its
-      // P by 2^(m_loc - m_row) <= 1 (rare).  Online-softmax state stays
-      // exact: l, O and P always share m_run.
-      const float own = sm::row_max64(s) * sl2;
-      const bool own_w = __any_sync(0xffffffffu, own > m_run + kRescaleThreshold);
-      const float m_loc = own_w ? fmaxf(m_run, own) : m_run;
+      const float pmax = sm::row_max64(s);
       float* red_t = red + ((j & 1) * 2 + g) * 2 * kBM;
-      red_t[h * kBM + r] = m_loc;
-      asm volatile("bar.arrive %0, 256;" ::"r"(3 + ((g * 2 + h) * 2 + (j & 1))) : "memory");
-      const int partner_bar = 3 + ((g * 2 + (h ^ 1)) * 2 + (j & 1));
-      float m_row;
-      if (!p.spec) {  // A/B knob (DMHA_SPEC=0): exchange first, then exponentials
-        asm volatile("bar.sync %0, 256;" ::"r"(partner_bar) : "memory");
-        m_row = fmaxf(m_loc, red_t[(h ^ 1) * kBM + r]);
-      } else {
-        m_row = m_loc;
+      red_t[h * kBM + r] = pmax;
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+      const float mt = fmaxf(pmax, red_t[(h ^ 1) * kBM + r]) * sl2;
+      const bool need = mt > m_run + kRescaleThreshold;
+      const bool warp_rescale = __any_sync(0xffffffffu, need);  // same in both halves
+      float alpha = 1.f;
+      if (warp_rescale) {
+        const float m_new = fmaxf(m_run, mt);
+        alpha = (m_new == -INFINITY) ? 1.f : ptx::ex2_approx(m_run - m_new);
+        l_run *= alpha;
+        m_run = m_new;
       }
-      const float m_use = (m_row == -INFINITY) ? 0.f : m_row;
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       if constexpr (kSepP) {
         // exponentials first, then wait for PV_g(j-1) to have read P_g(j-1)
         if (kEmu == 0 || masked)
           sm::exp_inplace64<0>(s, sl2, m_use);
         else
           sm::exp_inplace64<(kEmu > 4 ? 4 : kEmu)>(s, sl2, m_use);
-      } else {
-        sm::exp_inplace64<0>(s, sl2, m_use);
-      }
-      if (p.spec) {
-        asm volatile("bar.sync %0, 256;" ::"r"(partner_bar) : "memory");
-        m_row = fmaxf(m_loc, red_t[(h ^ 1) * kBM + r]);
-        if (__any_sync(0xffffffffu, m_row > m_loc)) {  // the partner half raised the max
-          const float f = m_row > m_loc ? ptx::ex2_approx(m_loc - m_row) : 1.f;
-#pragma unroll
-          for (int c = 0; c < 64; ++c) s[c] *= f;
+        if (j > 0) {
+          ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
+          ptx::tc_fence_after();
         }
+        l_run += sm::store_p64(s, tP);
+      } else {
+        l_run += sm::exp_half(s, sl2, m_use, tP);
       }
-      const bool warp_rescale = __any_sync(0xffffffffu, m_row != m_run);  // same in both halves
-      float alpha = 1.f;
-      if (warp_rescale) {
-        alpha = (m_row == m_run) ? 1.f : ptx::ex2_approx(m_run - m_row);
-        l_run *= alpha;
-        m_run = m_row;
-      }
-      if (kSepP && j > 0) {  // PV_g(j-1) has read P_g(j-1) (and finished O_g)
-        ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
-        ptx::tc_fence_after();
-      }
-      l_run += sm::store_p64(s, tP);
       if (warp_rescale && j > 0) {  // this half's D/2 columns of O
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -716,7 +690,6 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       // exponentials one after the other — WG1 starts tile j when WG0 has
       // finished it, WG0 starts tile j+1 when WG1 has finished tile j (named
       // barriers 1 = "WG0 may go", 2 = "WG1 may go"; 128 arrive + 128 sync).
-      // Measured within noise of the free-running default.
       const bool alt = !kSepP && p.alt;
       auto turn_wait = [&]() {
         if (alt && (g == 1 || j > 0)) asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
@@ -742,7 +715,6 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
-      turn_wait();
       const float mt = sm::row_max128(s) * sl2;
       const bool need = mt > m_run + kRescaleThreshold;
       const bool warp_rescale = __any_sync(0xffffffffu, need);
@@ -753,6 +725,9 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         l_run *= alpha;
         m_run = m_new;
       }
+      // only the exponential phase is serialised by the turn-taking: the S
+      // load and row max above overlap the other warpgroup's exponentials
+      turn_wait();
       // P = exp2(S*scale*log2e - m) -> bf16, written over the first 64 columns
       // of S (D = 64: into P_g) in 16-column chunks so the fp32 scores die as P
       // is produced.
@@ -951,8 +926,6 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
   p.kv_split = a.kv_split == 2 ? 2 : 1;
   p.n_mblk = static_cast<int>((a.Lq + 2 * kBM - 1) / (2 * kBM));
   p.lse_bias = a.lse_bias;
-  p.spec = 0;  // measured slower on the D = 64 split softmax
-  if (const char* e = std::getenv("DMHA_SPEC")) p.spec = std::atoi(e) != 0;
   p.alt = 0;
   if (const char* e = std::getenv("DMHA_ALT")) p.alt = std::atoi(e) != 0;
   p.trace = g_trace;
