@@ -48,6 +48,10 @@ WORKLOADS = {
     # A/B-only: C5's head shape at 1/8 of its length (tuning runs, not a bench line)
     "C5s": dict(L=131072, D=64, H=16, causal=True, dtype="bf16", layout="zigzag",
                 desc="C5-shaped A/B workload L=131072 D=64 H=16 bf16 causal"),
+    "C5nc": dict(L=131072, D=64, H=16, causal=False, dtype="bf16", layout="contiguous",
+                 desc="A/B workload L=131072 D=64 H=16 bf16 non-causal"),
+    "C2x4": dict(L=65536, D=64, H=8, causal=False, dtype="bf16", layout="contiguous",
+                 desc="A/B workload L=65536 D=64 H=8 bf16 non-causal (C2 heads, 4x longer)"),
 }
 METRIC = "attention TFLOP/s (4*L^2*D*H, /2 causal)"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}

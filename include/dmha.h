@@ -307,7 +307,8 @@ enum { DMHA_SCORER_L2 = 0, DMHA_SCORER_PROJ = 1 };
  * Never empty (R19): if no row on ANY rank passes, the highest-scoring row
  * over all ranks (ties: smallest global position under the init layout, with
  * L = n_rows * world_size) is kept by its owner.  Collective when
- * world_size > 1 (all ranks call with the same n_rows, width, scorer, tau).
+ * world_size > 1 (all ranks call with the same n_rows, width, scorer, tau;
+ * n_rows even for the zigzag layout, else DMHA_ERR_INVALID).
  * Outputs: x_out DEVICE [n_rows, width] bf16 capacity — the first *n_kept
  * rows are the kept rows; idx_out DEVICE [n_rows] int64 — the first *n_kept
  * entries are their LOCAL row indices, increasing (the re-aggregation map,
@@ -325,9 +326,12 @@ int dmha_select(const void *x, int64_t n_rows, int width, int scorer, const void
 int dmha_scatter_rows(const void *y_sel, const int64_t *idx, int64_t n_kept, int width,
                       void *y_full);
 
-/* Measurement hook: dev_buf (device, >= 4*9*64 uint64, or NULL to disable)
- * receives clock64 timeline stamps of the bf16 attention kernel (first 4 CTAs
- * of head 0, first 64 KV tiles; events documented in attn_fwd_sm100.cu). */
+/* Measurement hook: dev_buf (device, >= DMHA_TRACE_WORDS uint64, or NULL to
+ * disable) receives clock64 timeline stamps of the bf16 attention kernel
+ * (first 4 CTAs of head 0, first 64 KV tiles; events documented in
+ * attn_fwd_sm100.cu) and, from word 4096, %globaltimer (ns) at the start and
+ * end of each of the first 16384 CTAs (linear id x + y*gridDim.x + ...). */
+#define DMHA_TRACE_WORDS (4096 + 2 * 16384)
 int dmha_debug_set_trace(void *dev_buf);
 
 /* Block until all library work on the current stream is done (test helper). */

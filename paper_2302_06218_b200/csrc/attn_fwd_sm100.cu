@@ -132,6 +132,16 @@ __device__ __forceinline__ void trace_x(const Params& p, int ev, int j) {
     p.trace[(18 + ev) * 64 + j] = clock64();
 }
 
+// Per-CTA wall-clock stamps (%globaltimer, ns) at words 4096 + 2*id (+1).
+__device__ __forceinline__ void cta_stamp(const Params& p, int which) {
+  if (p.trace == nullptr) return;
+  const unsigned id = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (id >= 16384) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p.trace[4096 + 2 * id + which] = t;
+}
+
 __device__ __forceinline__ int64_t pos_of(const PosMap& m, int64_t i) {
   return i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
 }
@@ -234,6 +244,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
   }
+  if (threadIdx.x == 0) cta_stamp(p, 0);
   if (warp == kMmaWarp) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
@@ -887,6 +898,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
+  if (threadIdx.x == 0) cta_stamp(p, 1);
 }
 
 // ---------------------------------------------------------------- host side

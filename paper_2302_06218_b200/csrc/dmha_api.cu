@@ -1365,6 +1365,11 @@ int dmha_select(const void* x, int64_t n_rows, int width, int scorer, const void
   if (mis(x) || mis(x_out) || (psi && mis(psi)) || (reinterpret_cast<uintptr_t>(idx_out) & 7))
     return fail(DMHA_ERR_INVALID, "dmha_select: x/x_out/psi must be 16-byte aligned");
   if (g.dtype != DMHA_BF16) return fail(DMHA_ERR_UNSUPPORTED, "dmha_select: bf16 rows only");
+  // the tie-break maps local rows to global positions with the init layout:
+  // every rank holds the same n_rows (collective contract), two equal zigzag
+  // chunks of them when the layout is zigzag
+  if (g.world > 1 && g.layout == DMHA_LAYOUT_ZIGZAG && n_rows % 2)
+    return fail(DMHA_ERR_INVALID, "dmha_select: zigzag layout needs an even n_rows per rank");
   // workspace: flags | tile counts | tile offsets | 8 int64/double slots | scores
   const int64_t nb = dmha::selector_tiles(n_rows);
   const size_t off_counts = (static_cast<size_t>(n_rows) + 255) & ~size_t(255);

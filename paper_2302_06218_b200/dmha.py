@@ -419,8 +419,11 @@ def get_stats() -> dict:
     return {f: (float if t is ctypes.c_double else int)(getattr(s, f)) for f, t in Stats._fields_}
 
 
+TRACE_WORDS = 4096 + 2 * 16384  # DMHA_TRACE_WORDS (dmha.h)
+
+
 def debug_set_trace(buf):
-    """Timeline hook: buf = device uint64 tensor of >= 4*9*64 entries, or None."""
+    """Timeline hook: buf = device uint64 tensor of >= TRACE_WORDS entries, or None."""
     _check(lib().dmha_debug_set_trace(None if buf is None else _ptr(buf)))
 
 

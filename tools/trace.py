@@ -12,7 +12,7 @@ from paper_2302_06218_b200 import dmha  # noqa: E402
 L = int(os.environ.get("TL", 262144 // 8)); H = 16; D = int(os.environ.get("TD", 128))
 dmha.init(1, 0, None, 0, "bf16", "contiguous")
 q, k, v = (torch.randn(L, H, D, device="cuda").to(torch.bfloat16) for _ in range(3))
-buf = torch.zeros(4 * 9 * 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(dmha.TRACE_WORDS, dtype=torch.int64, device="cuda")
 dmha.forward(q, k, v, L, False)
 dmha.debug_set_trace(buf)
 dmha.forward(q, k, v, L, False)
