@@ -62,6 +62,9 @@ struct Roles {
   static constexpr int kThreads = (kSm + 4) * 32;
 };
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
+#ifndef DMHA_EXPFORM
+#define DMHA_EXPFORM 0  // D = 128 exponential loop: 0 scalar FFMA, 1 FFMA2/FADD2, 2 immediate-scale FFMA
+#endif
 #ifndef DMHA_SOFTMAX_REGS
 #define DMHA_SOFTMAX_REGS 0
 #endif
@@ -767,23 +770,43 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           l_run += sm::store_p(s, tP);
         }
       } else if (kEmu == 0 || masked) {
-        // scalar FFMA + MUFU.EX2 (the measured-fastest form on B200)
+#if DMHA_EXPFORM == 1
+        // packed FFMA2 / FADD2 (two scores per FMA-pipe instruction)
+        l_run += sm::exp_tile<0>(s, sl2, m_use, tP);
+#else
+        // scalar FFMA + MUFU.EX2; DMHA_EXPFORM == 2: the scale as an immediate
+        // (FFMA R, R, imm, R) and FADD2 sums
+#if DMHA_EXPFORM == 2
+        constexpr float kSl2 = D == 64 ? 0.18033688011112042f : 0.12751743082459868f;
+        float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#else
+        const float kSl2 = sl2;
         float sum0 = 0.f, sum1 = 0.f;
+#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], sl2, -m_use));
-            const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], sl2, -m_use));
+            const float e0 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e], kSl2, -m_use));
+            const float e1 = ptx::ex2_approx(fmaf(s[32 * c + 2 * e + 1], kSl2, -m_use));
+#if DMHA_EXPFORM == 2
+            acc2[e & 1] = __fadd2_rn(acc2[e & 1], make_float2(e0, e1));
+#else
             sum0 += e0;
             sum1 += e1;
+#endif
             __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
             pk[e] = *reinterpret_cast<uint32_t*>(&b);
           }
           ptx::tmem_st16(tP + c * 16, pk);
         }
+#if DMHA_EXPFORM == 2
+        l_run += (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
+#else
         l_run += sum0 + sum1;
+#endif
+#endif
       } else {
         l_run += sm::exp_tile<kEmu>(s, sl2, m_use, tP);
       }

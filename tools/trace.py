@@ -18,7 +18,7 @@ dmha.debug_set_trace(buf)
 dmha.forward(q, k, v, L, False)
 torch.cuda.synchronize()
 dmha.debug_set_trace(None)
-t = buf.view(4, 9, 64).cpu().numpy().astype(np.int64)
+t = buf[:4 * 9 * 64].view(4, 9, 64).cpu().numpy().astype(np.int64)
 for c in range(int(os.environ.get("TCTAS", 2))):
     tc = t[c] - t[c][0][0]
     print(f"CTA {c}: rows = tile j; cols = 0:WG0 saw S 1:WG0 P 2:WG1 saw S 3:WG1 P 4:mma saw P 5:mma PV issued 6:mma S issued 7:mma saw V landed 8:producer issued V load")

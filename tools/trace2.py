@@ -19,7 +19,7 @@ dmha.debug_set_trace(buf)
 dmha.forward(q, k, v, L, False)
 torch.cuda.synchronize()
 dmha.debug_set_trace(None)
-t = buf.view(4, 9, 64).cpu().numpy().astype(np.int64)
+t = buf[:4 * 9 * 64].view(4, 9, 64).cpu().numpy().astype(np.int64)
 tc = t[0] - t[0][0][0]
 print("cols: 0 WG0 saw S | 1 WG0 P | 2 WG1 saw S | 3 WG1 P | 4 S0,S1 issued | 5 PV saw P0 | 6 PV saw P1 | 7 WG0 S loaded | 8 WG0 exps start")
 for j in range(16, 26):
