@@ -105,14 +105,25 @@ int dmha_get_unique_id(void *id_out);
 /* world_size >= 1, 0 <= rank < world_size; unique_id NULL iff world_size == 1.
  * device: CUDA ordinal for this process; dtype: enum dmha_dtype; layout: enum
  * dmha_layout; cuda_stream: cudaStream_t (NULL = legacy default stream).
- * Collective over all ranks when world_size > 1 (ncclCommInitRank). */
+ * Collective over all ranks when world_size > 1.  K/V transport of the ring
+ * (env DMHA_TRANSPORT, read here): "nccl" (default) — ncclCommInitRank now;
+ * "peer" — every rank's K/V block is published in a
+ * library buffer shared by CUDA IPC and pulled by its consumers with the copy
+ * engine, ordered by interprocess events behind a host barrier in POSIX
+ * shared memory named after unique_id (ranks on one node); the
+ * NCCL communicator is then created on first use by a collective entry point
+ * (dmha_forward_headpar, dmha_select).  Errors: INVALID (arguments, unknown
+ * DMHA_TRANSPORT), UNSUPPORTED (not sm_100), CUDA, NCCL, STATE (shared-memory
+ * barrier failure or a rank missing for 300 s). */
 int dmha_init(int world_size, int rank, const void *unique_id, int device, int dtype,
               int layout, void *cuda_stream);
 
 /* Change the stream later calls are ordered on. */
 int dmha_set_stream(void *cuda_stream);
 
-/* Frees every library allocation and destroys the communicator. */
+/* Frees every library allocation, destroys the communicator and (peer
+ * transport) unmaps the peers' buffers after a host barrier.  Collective when
+ * world_size > 1. */
 int dmha_finalize(void);
 
 /* Thread-local message describing the last error ("" if none). */
@@ -124,7 +135,9 @@ const char *dmha_last_error(void);
  * [H, L_loc] fp32.  L is the GLOBAL length (L % P == 0; % 2P for ZIGZAG), D the
  * per-head dim (64 or 128), H >= 1 heads, causal 0/1.  All ranks must call with
  * identical (L, D, H, causal).  Ring: P-1 steps of ncclSend/ncclRecv of (K,V)
- * to rank+1 / from rank-1 overlapped with the local attention kernel, and an
+ * to rank+1 / from rank-1 (peer transport: a copy-engine pull of the block of
+ * step s+1 straight from its owner's published buffer) overlapped with the
+ * local attention kernel, and an
  * fp32 log-sum-exp combine of the per-step partials into a running
  * accumulator (north_star (3)) — for bf16 fused into the attention kernel's
  * epilogue (env DMHA_FUSED_COMBINE=0 selects the
@@ -329,8 +342,9 @@ int dmha_scatter_rows(const void *y_sel, const int64_t *idx, int64_t n_kept, int
 /* Measurement hook: dev_buf (device, >= DMHA_TRACE_WORDS uint64, or NULL to
  * disable) receives clock64 timeline stamps of the bf16 attention kernel
  * (first 4 CTAs of head 0, first 64 KV tiles; events documented in
- * attn_fwd_sm100.cu) and, from word 4096, %globaltimer (ns) at the start and
- * end of each of the first 16384 CTAs (linear id x + y*gridDim.x + ...). */
+ * attn_fwd_sm100.cu) and, from word 4096 and only in a library built with
+ * -DDMHA_CTA_STAMPS=1, %globaltimer (ns) at the start and end of each of the
+ * first 16384 CTAs (linear id x + y*gridDim.x + ...). */
 #define DMHA_TRACE_WORDS (4096 + 2 * 16384)
 int dmha_debug_set_trace(void *dev_buf);
 

@@ -136,14 +136,28 @@ __device__ __forceinline__ void trace_x(const Params& p, int ev, int j) {
 }
 
 // Per-CTA wall-clock stamps (%globaltimer, ns) at words 4096 + 2*id (+1).
+#ifndef DMHA_CTA_STAMPS
+#define DMHA_CTA_STAMPS 0  // measurement builds only: they cost the 96-register D = 64 kernel 20 %
+#endif
 __device__ __forceinline__ void cta_stamp(const Params& p, int which) {
-  if (p.trace == nullptr) return;
+  if (!DMHA_CTA_STAMPS || p.trace == nullptr) return;
   const unsigned id = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   if (id >= 16384) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   p.trace[4096 + 2 * id + which] = t;
 }
+
+// Sub-phase stamps of the D = 64 split softmax, compiled only into the
+// measurement build (-DDMHA_TRACE_PHASES=1, tools/trace.py via DMHA_LIB):
+// trace_x events 0-5 of the (g = 0, h = 0) warpgroup's thread 0.
+#ifndef DMHA_TRACE_PHASES
+#define DMHA_TRACE_PHASES 0
+#endif
+#define PHASE(ev)                                                                 \
+  do {                                                                            \
+    if (DMHA_TRACE_PHASES && g == 0 && h == 0 && threadIdx.x % 128 == 0) trace_x(p, ev, j); \
+  } while (0)
 
 __device__ __forceinline__ int64_t pos_of(const PosMap& m, int64_t i) {
   return i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
@@ -539,6 +553,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       ptx::tmem_ld32(tS + h * 64, *reinterpret_cast<float(*)[32]>(&s[0]));
       ptx::tmem_ld32(tS + h * 64 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
       ptx::tmem_wait_ld();
+      PHASE(0);
       if constexpr (kSepP) {
         ptx::tc_fence_before();
         ptx::mbar_arrive(&s_free[g]);
@@ -554,7 +569,9 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       const float pmax = sm::row_max64(s);
       float* red_t = red + ((j & 1) * 2 + g) * 2 * kBM;
       red_t[h * kBM + r] = pmax;
+      PHASE(1);
       asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+      PHASE(2);
       const float mt = fmaxf(pmax, red_t[(h ^ 1) * kBM + r]) * sl2;
       const bool need = mt > m_run + kRescaleThreshold;
       const bool warp_rescale = __any_sync(0xffffffffu, need);  // same in both halves
@@ -572,10 +589,12 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           sm::exp_inplace64<0>(s, sl2, m_use);
         else
           sm::exp_inplace64<(kEmu > 4 ? 4 : kEmu)>(s, sl2, m_use);
+        PHASE(3);
         if (j > 0) {
           ptx::mbar_wait(&pv_done[g], static_cast<uint32_t>((j - 1) & 1));
           ptx::tc_fence_after();
         }
+        PHASE(4);
         l_run += sm::store_p64(s, tP);
       } else {
         l_run += sm::exp_half(s, sl2, m_use, tP);
@@ -592,6 +611,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         }
       }
       ptx::tmem_wait_st();
+      PHASE(5);
       ptx::tc_fence_before();
       if (h == 0 && threadIdx.x % 128 == 0) trace_stamp(p, 2 * g + 1, j);
       ptx::mbar_arrive(&p_ready[g]);

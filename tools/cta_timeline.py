@@ -3,7 +3,11 @@ CTA start / end, dmha_debug_set_trace): CTA durations, launch gaps on an SM
 slot, and the steady-state time per KV tile — separates per-CTA fixed cost
 from the tile loop.
 
-    TL=16384 TH=8 TD=64 [TC=0] python tools/cta_timeline.py
+    python -m paper_2302_06218_b200.build --variant tr -DDMHA_TRACE_PHASES=1 -DDMHA_CTA_STAMPS=1
+    DMHA_LIB=paper_2302_06218_b200/ab/tr/libdmha.so TL=16384 TH=8 TD=64 [TC=0] python tools/cta_timeline.py
+
+The stamps exist only in a measurement build (-DDMHA_CTA_STAMPS=1): in the
+product they cost the 96-register D = 64 kernel 20 %.
 """
 import os
 import sys

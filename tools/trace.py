@@ -49,6 +49,15 @@ if D == 128 and x[0][10]:
         ph = [np.mean([x[9 * g + e][j] - (saw[j] if e == 0 else x[9 * g + e - 1][j]) for j in js]) for e in range(4)]
         pr = np.mean([t[0][2 * g + 1][j] - x[9 * g + 3][j] for j in js])
         print(f"  WG{g}: load+max {ph[0]:.0f}  turn-wait {ph[1]:.0f}  exps {ph[2]:.0f}  pack+store {ph[3]:.0f}  ->P-ready {pr:.0f}")
+elif D == 64 and os.environ.get("TPHASES") and x[0][10]:
+    # split-softmax sub-phases (measurement build -DDMHA_TRACE_PHASES=1): WG (g0,h0)
+    js = range(8, 60)
+    saw = t[0][0]
+    seg = [("S load", lambda j: x[0][j] - saw[j]), ("mask+max+smem", lambda j: x[1][j] - x[0][j]),
+           ("bar.sync", lambda j: x[2][j] - x[1][j]), ("decision+exps", lambda j: x[3][j] - x[2][j]),
+           ("pv_done wait", lambda j: x[4][j] - x[3][j]), ("store P+sum", lambda j: x[5][j] - x[4][j]),
+           ("-> next S", lambda j: saw[j + 1] - x[5][j])]
+    print("  split softmax (g0 h0) per tile: " + "  ".join(f"{n} {np.mean([f(j) for j in js]):.0f}" for n, f in seg))
 elif x[0][10]:
     x0 = t[0][0][0]
     names = ["g0 preK", "g0 Kland", "g0 sfree", "g0 Vland", "g0 PVdone", "prodK pre", "prodK free", "", "",
