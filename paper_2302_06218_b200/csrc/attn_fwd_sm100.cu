@@ -73,6 +73,7 @@ constexpr int kOtherRegs = kSmRegs > 0 ? ((384 * 168 - 256 * kSmRegs) / 128) / 8
 static_assert(kSmRegs == 0 || (kSmRegs % 8 == 0 && kSmRegs <= 256 && kOtherRegs >= 24),
               "setmaxnreg budget");
 
+
 // kPS (D = 128 only): P_g(j) goes to shared memory instead of over S_g's TMEM
 // columns, so QK^T(j+1) can run during softmax(j) (the separate-P schedule of
 // D = 64, whose P fits in TMEM).  Shared memory then holds Q (2 tiles), ONE K
