@@ -345,13 +345,15 @@ def test_error_codes(lib_bf16):
     assert e.value.code == dmha.ERR_INVALID
 
 
-@pytest.mark.parametrize("P", [2, 4])
+# (P, H, D): row segments of H/P heads x D bf16 = 16 vectors (flat copy path),
+# 64 vectors and 24 vectors (not a power of two: warp-per-row path)
+@pytest.mark.parametrize("P,H,D", [(2, 4, 64), (4, 4, 128), (2, 8, 128), (2, 6, 64)])
 @pytest.mark.parametrize("layout", ["contiguous", "zigzag"])
 @pytest.mark.parametrize("causal", [False, True])
-def test_headpar_emulated_matches_oracle_and_ring(lib_bf16, oracle_mod, P, layout, causal):
+def test_headpar_emulated_matches_oracle_and_ring(lib_bf16, oracle_mod, P, H, D, layout, causal):
     """NEXT-1, the paper's own exchange: head-parallel all-to-all
     path vs the oracle, and vs the ring (two distributions, one result)."""
-    L, H, D = 2048 + 128 * P, 4, 64 if P == 2 else 128
+    L = 2048 + 128 * P
     q, k, v = inputs.qkv(L, H, D, seed=600 + P)
     parts = [np.stack([dmha.shard(x, P, r, layout) for r in range(P)]) for x in (q, k, v)]
     dq, dk, dv = (to_dev(p) for p in parts)
@@ -377,7 +379,7 @@ def test_headpar_requires_divisible_heads(lib_bf16):
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("D", [64, 128])
 def test_mha_layer_matches_oracle(lib_bf16, oracle_mod, causal, D):
-    """NEXT-3: the full layer (cuBLAS projections + our attention) vs the
+    """NEXT-3: the full layer (tcgen05 projection GEMMs + our attention) vs the
     oracle layer with the same bf16 storage points (reading R17)."""
     L, H, d_model = 1000, 4, 256
     x, wq, wk, wv, wo = inputs.mha_layer(L, d_model, H, D)
