@@ -62,6 +62,12 @@ struct Roles {
   static constexpr int kThreads = (kSm + 4) * 32;
 };
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale when max grows by > 2^8
+#ifndef DMHA_KST64
+#define DMHA_KST64 3  // D = 64 K ring slots
+#endif
+#ifndef DMHA_VST64
+#define DMHA_VST64 3  // D = 64 V ring slots
+#endif
 #ifndef DMHA_EXPFORM
 #define DMHA_EXPFORM 0  // D = 128 exponential loop: 0 scalar FFMA, 1 FFMA2/FADD2, 2 immediate-scale FFMA
 #endif
@@ -86,8 +92,8 @@ struct Cfg {
   // Separate-P schedule: K and V in their own rings (kKSt / kVSt slots);
   // otherwise one K/V ring of kStages slots (K_j, V_j alternate).
   static constexpr bool kSepP = (D == 64) || kPS;
-  static constexpr int kKSt = (D == 64) ? 3 : 1;
-  static constexpr int kVSt = (D == 64) ? 3 : 2;
+  static constexpr int kKSt = (D == 64) ? DMHA_KST64 : 1;
+  static constexpr int kVSt = (D == 64) ? DMHA_VST64 : 2;
   static constexpr int kStages = kSepP ? kKSt + kVSt : 4;
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = 2 * kTileBytes;
