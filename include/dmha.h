@@ -238,6 +238,16 @@ int dmha_workspace_bytes(int64_t L, int D, int H, size_t *bytes_out);
  * holds, which runs each rank with one set of ring buffers). */
 int dmha_ring_workspace_bytes(int world_size, int64_t L, int D, int H, size_t *bytes_out);
 
+/* Allocate now the workspace a forward of global length L (D, H) at
+ * world_size needs (dmha_ring_workspace_bytes; world_size = the init world
+ * size for dmha_forward, P for dmha_forward_emulated), so that later forwards
+ * of that size or smaller allocate nothing: no implicit device
+ * synchronisation inside a forward, and the forward can be captured into a
+ * CUDA graph (stream capture; the ring's comm stream joins the capture
+ * through its events).  Collective with the peer transport.  Errors: STATE,
+ * INVALID, UNSUPPORTED (D), OOM. */
+int dmha_reserve(int world_size, int64_t L, int D, int H);
+
 /* SURVEY §8(c) "Accounting" and §8(d): synchronises outstanding profiled
  * work, then copies the counters into *s (caller-owned).  INVALID if null. */
 int dmha_get_stats(struct dmha_stats *s);

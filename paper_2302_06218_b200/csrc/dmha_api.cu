@@ -877,6 +877,26 @@ int dmha_ring_workspace_bytes(int world_size, int64_t L, int D, int H, size_t* b
   return DMHA_OK;
 }
 
+int dmha_reserve(int world_size, int64_t L, int D, int H) {
+  if (int rc = check_state()) return rc;
+  if (world_size < 1 || L < 1 || H < 1 || L % world_size)
+    return fail(DMHA_ERR_INVALID, "dmha_reserve: bad args");
+  if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_reserve: D=%d", D);
+  const int64_t Lloc = L / world_size;
+  if (world_size == 1) {
+    if (split_kv_active(Lloc, D, H)) return ensure_ring_ws(Lloc, D, H, false, true);
+    return DMHA_OK;
+  }
+  if (int rc = ensure_ring_ws(Lloc, D, H, true)) return rc;
+  if (g.peer && world_size == g.world) {
+    std::string err;
+    const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+    if (int rc = dmha::peer_ensure_pub(g.peer, 2 * blk, &err)) return fail(rc, "%s", err.c_str());
+    update_ws_stat();
+  }
+  return DMHA_OK;
+}
+
 int dmha_get_stats(dmha_stats* s) {
   if (!s) return fail(DMHA_ERR_INVALID, "dmha_get_stats: null");
   resolve_profiles();

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
     "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
     "dmha_forward_headpar", "dmha_forward_headpar_emulated", "dmha_mha_forward", "dmha_linear",
+    "dmha_reserve",
     "dmha_select", "dmha_scatter_rows", "dmha_ring_workspace_bytes",
 )
 
@@ -99,6 +100,7 @@ def lib():
             "dmha_forward_headpar_emulated": [I, I, P, P, P, P, P, I64, I, I, I],
             "dmha_mha_forward": [P, P, P, P, P, P, P, I64, I, I, I, I],
             "dmha_linear": [P, P, P, I64, I, I],
+            "dmha_reserve": [I, I64, I, I],
             "dmha_select": [P, I64, I, I, P, ctypes.c_double, P, P, P, ctypes.POINTER(I64)],
             "dmha_scatter_rows": [P, P, I64, I, P],
         }
@@ -192,6 +194,7 @@ def init(world_size: int = 1, rank: int = 0, unique_id: bytes | None = None, dev
     _check(lib().dmha_init(world_size, rank, None if uid is None else ctypes.addressof(uid), device,
                            dtype_code(dtype), layout_code(layout), s))
     _STATE["dtype"] = dtype_code(dtype)
+    _STATE["world"] = int(world_size)
 
 
 def init_distributed(dtype="bf16", layout="contiguous", device: int | None = None):
@@ -425,6 +428,12 @@ TRACE_WORDS = 4096 + 2 * 16384  # DMHA_TRACE_WORDS (dmha.h)
 def debug_set_trace(buf):
     """Timeline hook: buf = device uint64 tensor of >= TRACE_WORDS entries, or None."""
     _check(lib().dmha_debug_set_trace(None if buf is None else _ptr(buf)))
+
+
+def reserve(L: int, D: int, H: int, world_size: int | None = None):
+    """Pre-allocate the workspace of a forward of this size (CUDA-graph capture)."""
+    ws = world_size if world_size is not None else _STATE.get("world", 1)
+    _check(lib().dmha_reserve(int(ws), int(L), int(D), int(H)))
 
 
 def set_profiling(enable: bool):

@@ -528,3 +528,52 @@ def test_fp32_tf32x3_beats_one_pass_tf32_bound(oracle_mod):
     ref_o, _ = oracle_mod.attention(q, k, v, False)
     _, rel = metrics(out, ref_o)
     assert rel <= 1e-5, rel
+
+
+@pytest.mark.parametrize("case", ["p1_split", "p1_large_grid", "emulated_p4"])
+def test_forward_captures_into_cuda_graph(lib_bf16, case):
+    """After dmha_reserve, a forward allocates nothing and is stream-ordered
+    only, so it captures into a CUDA graph — at P = 1 (split-KV small grid:
+    attention + combine; large grid: one launch) and the emulated P = 4 ring
+    (comm stream, copies and events join the capture).  Replays on new input
+    values equal eager forwards bit for bit."""
+    if case == "p1_split":
+        P, L, H, D, causal, layout = 1, 5000, 3, 64, False, "contiguous"
+    elif case == "p1_large_grid":
+        P, L, H, D, causal, layout = 1, 65536, 4, 128, True, "contiguous"
+    else:
+        P, L, H, D, causal, layout = 4, 4096, 2, 128, True, "zigzag"
+    shape = (L, H, D) if P == 1 else (P, L // P, H, D)
+    lshape = (H, L) if P == 1 else (P, H, L // P)
+    q, k, v = (torch.empty(shape, dtype=torch.bfloat16, device="cuda") for _ in range(3))
+    out = torch.empty_like(q)
+    lse = torch.empty(lshape, dtype=torch.float32, device="cuda")
+    dmha.reserve(L, D, H, world_size=P)
+
+    def fwd():
+        if P == 1:
+            dmha.forward(q, k, v, L, causal, out, lse)
+        else:
+            dmha.forward_emulated(P, layout, q, k, v, L, causal, out, lse)
+
+    gen = torch.Generator(device="cuda").manual_seed(17)
+    for x in (q, k, v):
+        x.copy_(torch.randn(shape, generator=gen, device="cuda"))
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fwd()  # warm-up outside the capture (function attributes, descriptors)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        fwd()
+    for seed in (21, 22):
+        for x in (q, k, v):
+            x.copy_(torch.randn(shape, generator=gen.manual_seed(seed), device="cuda"))
+        graph.replay()
+        torch.cuda.synchronize()
+        g_o, g_l = out.clone(), lse.clone()
+        fwd()
+        torch.cuda.synchronize()
+        assert torch.equal(g_o, out) and torch.equal(g_l, lse), f"{case} seed {seed}"
