@@ -132,7 +132,9 @@ const char *dmha_last_error(void);
 /* ---- the distributed forward -------------------- */
 
 /* q, k, v, out: DEVICE pointers to this rank's [L_loc, H, D] shard; lse: DEVICE
- * [H, L_loc] fp32.  L is the GLOBAL length (L % P == 0; % 2P for ZIGZAG), D the
+ * [H, L_loc] fp32, L_loc = dmha_shard_rows(L, P, rank, layout).  L is the
+ * GLOBAL length (any L >= 1 for CONTIGUOUS — uneven shards differ by one row
+ * and the ring moves each block at its owner's size; L % 2P == 0 for ZIGZAG), D the
  * per-head dim (64 or 128), H >= 1 heads, causal 0/1.  All ranks must call with
  * identical (L, D, H, causal).  Ring: P-1 steps of ncclSend/ncclRecv of (K,V)
  * to rank+1 / from rank-1 (peer transport: a copy-engine pull of the block of
@@ -167,8 +169,11 @@ int dmha_forward_host(const void *q, const void *k, const void *v, void *out, fl
                       int64_t L, int D, int H, int causal);
 
 /* Single-GPU emulation of the P-rank ring (test/measurement hook): q/k/v/out
- * are DEVICE [P][L_loc, H, D] buffers holding every rank's shard back to back
- * (rank-major), lse is [P][H, L_loc].  Runs each rank's ring in turn through
+ * are DEVICE [P][Lm, H, D] buffers holding every rank's shard back to back
+ * (rank-major), lse is [P][H*Lm], Lm = the largest shard (ceil(L/P) for
+ * CONTIGUOUS); slot r holds rank r's dmha_shard_rows rows first and its lse
+ * as [H, rows] packed from the slot start (for even shards simply
+ * [P][Lm, H, D] and [P][H, Lm]).  Runs each rank's ring in turn through
  * the SAME loop as dmha_forward at world_size P — the two K/V ring buffers,
  * the comm stream, the recv/compute events and the buffer-reuse rule — with a
  * single-GPU transport: each receive is one cudaMemcpyAsync per K and per V
@@ -289,6 +294,12 @@ int dmha_ring_plan_step(int world_size, int rank, int step, int layout, int64_t 
  * (L, P, layout).  Pure host index math. Returns INVALID on bad arguments. */
 int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_t i,
                          int64_t *global_out);
+
+/* a1 ("equal as possible"): the number of rows rank r
+ * owns — CONTIGUOUS: L/P, plus one for the first L % P ranks (L need not be
+ * divisible by P; rank r starts at r*(L/P) + min(r, L % P)); ZIGZAG: L/P
+ * (L % 2P == 0 required).  Host index math; INVALID on bad arguments. */
+int dmha_shard_rows(int64_t L, int world_size, int rank, int layout, int64_t *rows_out);
 
 /* a2 (P:193-211 + P:672-674): one local flash-attention pass of this rank's
  * query block against one K/V block, on the dmha_init stream.

@@ -300,6 +300,17 @@ int ensure_ring_ws(int64_t Lloc, int D, int H, bool need_kv, bool force_part = f
   return DMHA_OK;
 }
 
+// Shard sizes ("equal as possible"):
+// contiguous — rank r owns L/P rows, plus one of the first L % P ranks;
+// zigzag — 2 chunks of L/(2P) rows (L % 2P == 0 required).
+int64_t shard_rows(int64_t L, int P, int r, int layout) {
+  if (layout == DMHA_LAYOUT_ZIGZAG) return L / P;
+  return L / P + (r < L % P ? 1 : 0);
+}
+int64_t max_shard_rows(int64_t L, int P, int layout) {
+  return layout == DMHA_LAYOUT_ZIGZAG ? L / P : (L + P - 1) / P;
+}
+
 dmha::PosMap posmap(int64_t L, int P, int r, int layout) {
   dmha::PosMap m;
   if (layout == DMHA_LAYOUT_ZIGZAG) {
@@ -308,10 +319,10 @@ dmha::PosMap posmap(int64_t L, int P, int r, int layout) {
     m.base1 = static_cast<int64_t>(2 * P - 1 - r) * c;
     m.chunk = c;
   } else {
-    const int64_t Lloc = L / P;
-    m.base0 = r * Lloc;
-    m.base1 = r * Lloc + Lloc;
-    m.chunk = Lloc;
+    const int64_t rows = shard_rows(L, P, r, layout);
+    m.base0 = r * (L / P) + std::min<int64_t>(r, L % P);
+    m.base1 = m.base0 + rows;
+    m.chunk = rows;
   }
   return m;
 }
@@ -322,21 +333,23 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   return pa < pb + nb && pb < pa + na;
 }
 
-// nshards: how many [L_loc, H, D] shards each buffer holds back to back (the
-// emulated entry points pass P rank-major shards), for the overlap check.
+// nshards: how many shards each buffer holds back to back (the emulated entry
+// points pass P rank-major shards of max_shard_rows rows), for the overlap
+// check; rows: the rows of one shard (this rank's by default).
 int validate(const void* q, const void* k, const void* v, const void* out, const float* lse,
-             int64_t L, int D, int H, int P, int layout, int nshards = 1) {
+             int64_t L, int D, int H, int P, int layout, int nshards = 1, int64_t rows = -1) {
   if (!q || !k || !v || !out || !lse) return fail(DMHA_ERR_INVALID, "dmha: null pointer");
   if (L < 1 || H < 1) return fail(DMHA_ERR_INVALID, "dmha: need L >= 1 and H >= 1");
   if (D != 64 && D != 128)
     return fail(DMHA_ERR_UNSUPPORTED, "dmha: per-head dim D=%d unsupported (64 or 128)", D);
   if (layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG)
     return fail(DMHA_ERR_INVALID, "dmha: unknown layout %d", layout);
-  const int64_t div = layout == DMHA_LAYOUT_ZIGZAG ? 2LL * P : P;
-  if (L % div != 0)
-    return fail(DMHA_ERR_INVALID, "dmha: L=%lld not divisible by %lld (world %d, layout %d)",
-                static_cast<long long>(L), static_cast<long long>(div), P, layout);
-  const int64_t Lloc = L / P;
+  if (layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * P) != 0)
+    return fail(DMHA_ERR_INVALID, "dmha: L=%lld not divisible by 2P=%d (zigzag layout)",
+                static_cast<long long>(L), 2 * P);
+  // contiguous shards may be uneven (L % P != 0): the first L % P ranks hold
+  // one row more
+  const int64_t Lloc = rows >= 0 ? rows : max_shard_rows(L, P, layout);
   if (Lloc > (1LL << 31) - 1) return fail(DMHA_ERR_INVALID, "dmha: L/P too large");
   const void* ptrs[5] = {q, k, v, out, lse};
   for (const void* p : ptrs)
@@ -429,8 +442,9 @@ dmha_ring_plan make_plan(int P, int r, int s, int layout, int64_t L) {
 // so both run identical kernels in identical order).
 int ring_compute_step(int s, int P, int r, int layout, const void* q, const void* ks,
                       const void* vs, void* out, float* lse, int64_t L, int D, int H, int causal) {
-  const int64_t Lloc = L / P;
   const dmha_ring_plan pl = make_plan(P, r, s, layout, L);
+  const int64_t Lloc = shard_rows(L, P, r, layout);    // query rows (this rank)
+  const int64_t Lkv = shard_rows(L, P, pl.src, layout);  // key rows (the block's owner)
   const dmha::PosMap qm{pl.q_base0, pl.q_base1, pl.q_chunk}, km{pl.k_base0, pl.k_base1, pl.k_chunk};
   switch (pl.output) {
     case DMHA_PLAN_FINAL: {
@@ -438,24 +452,24 @@ int ring_compute_step(int s, int P, int r, int layout, const void* q, const void
       // idle in the last wave: split each row block's keys over two CTAs
       // and merge the two fp32 partials with the log-sum-exp combine.
       if (!split_kv_active(Lloc, D, H))
-        return run_local(q, ks, vs, out, lse, Lloc, Lloc, D, H, causal, qm, km, dmha::OUT_FINAL);
-      if (int rc = ensure_ring_ws(Lloc, D, H, false, true)) return rc;
-      if (int rc = run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
+        return run_local(q, ks, vs, out, lse, Lloc, Lkv, D, H, causal, qm, km, dmha::OUT_FINAL);
+      if (int rc = ensure_ring_ws(Lloc, D, H, false, true)) return rc;  // P = 1: Lkv == Lloc
+      if (int rc = run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lkv, D, H, causal, qm, km,
                              dmha::OUT_PARTIAL_F32, nullptr, nullptr, 2, g.o_part, g.lse_part))
         return rc;
       return run_combine(g.o_part, g.lse_part, out, lse, Lloc, D, H, 1);
     }
     case DMHA_PLAN_ACC:
-      return run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lloc, D, H, causal, qm, km,
+      return run_local(q, ks, vs, g.o_acc, g.lse_acc, Lloc, Lkv, D, H, causal, qm, km,
                        dmha::OUT_PARTIAL_F32);
     default: {
       const bool fin = pl.output == DMHA_PLAN_COMBINE_FINAL;
       if (fused_combine(D))  // NEXT-2: merge inside the attention epilogue
         return run_local(q, ks, vs, fin ? out : static_cast<void*>(g.o_acc), fin ? lse : g.lse_acc,
-                         Lloc, Lloc, D, H, causal, qm, km,
+                         Lloc, Lkv, D, H, causal, qm, km,
                          fin ? dmha::OUT_COMBINE_FINAL : dmha::OUT_COMBINE_ACC, g.o_acc,
                          g.lse_acc);
-      int rc = run_local(q, ks, vs, g.o_part, g.lse_part, Lloc, Lloc, D, H, causal, qm, km,
+      int rc = run_local(q, ks, vs, g.o_part, g.lse_part, Lloc, Lkv, D, H, causal, qm, km,
                          dmha::OUT_PARTIAL_F32);
       if (rc) return rc;
       return run_combine(g.o_part, g.lse_part, out, lse, Lloc, D, H,
@@ -496,58 +510,65 @@ int poll_nccl() {
 //   CopyTransport  the single-GPU emulation (dmha_forward_emulated): one
 //                  cudaMemcpyAsync per K / V block from the shard rank r-1
 //                  holds at step s (rank (r-1-s) mod P's original block).
+// Block sizes: the block of ring step s belongs to rank src_s and holds its
+// shard_rows(src_s) rows (uneven contiguous shards differ by one row); a ring
+// buffer holds K at offset 0 and V at offset vo (the largest block's bytes).
 struct Transport {
   virtual ~Transport() = default;
   virtual int exchange(const dmha_ring_plan& pl, int s, const void* kcur, const void* vcur,
-                       char* dst, size_t blk) = 0;
+                       size_t send_bytes, char* dst, size_t recv_bytes, size_t vo) = 0;
 };
 
 struct NcclTransport final : Transport {
-  int exchange(const dmha_ring_plan& pl, int, const void* kcur, const void* vcur, char* dst,
-               size_t blk) override {
+  int exchange(const dmha_ring_plan& pl, int, const void* kcur, const void* vcur, size_t send_bytes,
+               char* dst, size_t recv_bytes, size_t vo) override {
     CK_NCCL(ncclGroupStart());
-    CK_NCCL(ncclSend(kcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
-    CK_NCCL(ncclSend(vcur, blk, ncclChar, pl.send_to, g.nccl, g.comm));
-    CK_NCCL(ncclRecv(dst, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
-    CK_NCCL(ncclRecv(dst + blk, blk, ncclChar, pl.recv_from, g.nccl, g.comm));
+    CK_NCCL(ncclSend(kcur, send_bytes, ncclChar, pl.send_to, g.nccl, g.comm));
+    CK_NCCL(ncclSend(vcur, send_bytes, ncclChar, pl.send_to, g.nccl, g.comm));
+    CK_NCCL(ncclRecv(dst, recv_bytes, ncclChar, pl.recv_from, g.nccl, g.comm));
+    CK_NCCL(ncclRecv(dst + vo, recv_bytes, ncclChar, pl.recv_from, g.nccl, g.comm));
     CK_NCCL(ncclGroupEnd());
     return DMHA_OK;
   }
 };
 
 struct CopyTransport final : Transport {
-  const char *k_all, *v_all;  // [P][L_loc, H, D] shards, rank-major
-  size_t shard;
+  const char *k_all, *v_all;  // [P][max shard rows, H, D] shards, rank-major
+  size_t shard;               // bytes per shard slot
   int P, r, layout;
   int64_t L;
   CopyTransport(const char* k, const char* v, size_t sh, int P_, int r_, int lay, int64_t L_)
       : k_all(k), v_all(v), shard(sh), P(P_), r(r_), layout(lay), L(L_) {}
-  int exchange(const dmha_ring_plan& pl, int s, const void*, const void*, char* dst,
-               size_t blk) override {
+  int exchange(const dmha_ring_plan& pl, int s, const void*, const void*, size_t, char* dst,
+               size_t recv_bytes, size_t vo) override {
     // what rank recv_from sends at step s is the block it attends at step s,
     // i.e. rank (recv_from - s) mod P's shard == the src of our step s+1
     const int src_next = make_plan(P, r, s + 1, layout, L).src;
     if (src_next != ((pl.recv_from - s) % P + P) % P)
       return fail(DMHA_ERR_STATE, "dmha: ring plan inconsistent at rank %d step %d", r, s);
-    CK_CUDA(cudaMemcpyAsync(dst, k_all + src_next * shard, blk, cudaMemcpyDeviceToDevice, g.comm));
-    CK_CUDA(cudaMemcpyAsync(dst + blk, v_all + src_next * shard, blk, cudaMemcpyDeviceToDevice,
+    CK_CUDA(cudaMemcpyAsync(dst, k_all + src_next * shard, recv_bytes, cudaMemcpyDeviceToDevice,
                             g.comm));
+    CK_CUDA(cudaMemcpyAsync(dst + vo, v_all + src_next * shard, recv_bytes,
+                            cudaMemcpyDeviceToDevice, g.comm));
     return DMHA_OK;
   }
 };
 
 // NEXT-2 peer transport: the block of ring step s+1 is rank src_next's own
-// K/V, which that rank published in its IPC-shared buffer at the start of the
-// forward (see peer_forward); pull it with the copy engine once its
-// "published" event has fired.  No relay: each block crosses the link once.
+// K/V, which that rank published in its IPC-shared buffer (K at 0, V at vo)
+// at the start of the forward (see peer_forward); pull it with the copy
+// engine once its "published" event has fired.  No relay: each block crosses
+// the link once.
 struct PeerTransport final : Transport {
   int P, r;
   PeerTransport(int P_, int r_) : P(P_), r(r_) {}
-  int exchange(const dmha_ring_plan&, int s, const void*, const void*, char* dst,
-               size_t blk) override {
+  int exchange(const dmha_ring_plan&, int s, const void*, const void*, size_t, char* dst,
+               size_t recv_bytes, size_t vo) override {
     const int src_next = ((r - s - 1) % P + P) % P;
+    const char* pub = static_cast<const char*>(dmha::peer_pub(g.peer, src_next));
     CK_CUDA(cudaStreamWaitEvent(g.comm, dmha::peer_pub_event(g.peer, src_next), 0));
-    CK_CUDA(cudaMemcpyAsync(dst, dmha::peer_pub(g.peer, src_next), 2 * blk, cudaMemcpyDefault, g.comm));
+    CK_CUDA(cudaMemcpyAsync(dst, pub, recv_bytes, cudaMemcpyDefault, g.comm));
+    CK_CUDA(cudaMemcpyAsync(dst + vo, pub + vo, recv_bytes, cudaMemcpyDefault, g.comm));
     return DMHA_OK;
   }
 };
@@ -577,9 +598,9 @@ void count_sent(uint64_t bytes) {
 int ring_forward(int P, int r, int layout, const void* q, const void* k, const void* v, void* out,
                  float* lse, int64_t L, int D, int H, int causal, Transport& tx) {
   if (P == 1) return ring_compute_step(0, 1, 0, layout, q, k, v, out, lse, L, D, H, causal);
-  const int64_t Lloc = L / P;
-  if (int rc = ensure_ring_ws(Lloc, D, H, true)) return rc;
-  const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+  if (int rc = ensure_ring_ws(max_shard_rows(L, P, layout), D, H, true)) return rc;
+  const size_t row_bytes = static_cast<size_t>(H) * D * elem_bytes(g.dtype);
+  const size_t vo = static_cast<size_t>(max_shard_rows(L, P, layout)) * row_bytes;  // V offset
   CK_CUDA(cudaEventRecord(g.ev_start, g.stream));
   CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_start, 0));
   const void* kcur = k;
@@ -593,13 +614,19 @@ int ring_forward(int P, int r, int layout, const void* q, const void* k, const v
       const int nb = pl.recv_buf;
       if (pl.recv_after_compute_of >= 0) CK_CUDA(cudaStreamWaitEvent(g.comm, g.ev_done[nb], 0));
       char* dst = static_cast<char*>(g.kvbuf[nb]);
-      int rc = timed(2, g.comm, [&]() { return tx.exchange(pl, s, kcur, vcur, dst, blk); });
+      const size_t send_bytes = static_cast<size_t>(shard_rows(L, P, pl.src, layout)) * row_bytes;
+      const size_t recv_bytes =
+          static_cast<size_t>(shard_rows(L, P, make_plan(P, r, s + 1, layout, L).src, layout)) *
+          row_bytes;
+      int rc = timed(2, g.comm, [&]() {
+        return tx.exchange(pl, s, kcur, vcur, send_bytes, dst, recv_bytes, vo);
+      });
       if (rc) {
         nvtxRangePop();
         return rc;
       }
       CK_CUDA(cudaEventRecord(g.ev_recv[nb], g.comm));
-      count_sent(2 * blk);
+      count_sent(2 * send_bytes);
     }
     int rc = ring_compute_step(s, P, r, layout, q, kcur, vcur, out, lse, L, D, H, causal);
     nvtxRangePop();
@@ -610,7 +637,7 @@ int ring_forward(int P, int r, int layout, const void* q, const void* k, const v
       const int nb = pl.recv_buf;
       CK_CUDA(cudaStreamWaitEvent(g.stream, g.ev_recv[nb], 0));
       kcur = g.kvbuf[nb];
-      vcur = static_cast<char*>(g.kvbuf[nb]) + blk;
+      vcur = static_cast<char*>(g.kvbuf[nb]) + vo;
     }
   }
   // The comm stream's last work must be ordered before any later reuse.
@@ -746,7 +773,9 @@ int headpar_rank(int P, int r, int layout, const void* q, const void* k, const v
 int validate_headpar(int P, int64_t L, int H) {
   if (P < 1 || H % P != 0)
     return fail(DMHA_ERR_INVALID, "dmha headpar: H=%d must be divisible by the world size %d", H, P);
-  (void)L;
+  if (L % P != 0)  // the all-to-all blocks are uniform
+    return fail(DMHA_ERR_INVALID, "dmha headpar: L=%lld must be divisible by the world size %d",
+                static_cast<long long>(L), P);
   return DMHA_OK;
 }
 
@@ -870,19 +899,20 @@ int dmha_workspace_bytes(int64_t L, int D, int H, size_t* bytes_out) {
 
 int dmha_ring_workspace_bytes(int world_size, int64_t L, int D, int H, size_t* bytes_out) {
   if (int rc = check_state()) return rc;
-  if (!bytes_out || world_size < 1 || L < 1 || H < 1 || L % world_size)
+  if (!bytes_out || world_size < 1 || L < 1 || H < 1 ||
+      (g.layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * world_size)))
     return fail(DMHA_ERR_INVALID, "dmha_workspace_bytes: bad args");
   if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_workspace_bytes: D=%d", D);
-  *bytes_out = ring_ws_bytes(world_size, L / world_size, D, H);
+  *bytes_out = ring_ws_bytes(world_size, max_shard_rows(L, world_size, g.layout), D, H);
   return DMHA_OK;
 }
 
 int dmha_reserve(int world_size, int64_t L, int D, int H) {
   if (int rc = check_state()) return rc;
-  if (world_size < 1 || L < 1 || H < 1 || L % world_size)
+  if (world_size < 1 || L < 1 || H < 1 || (g.layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * world_size)))
     return fail(DMHA_ERR_INVALID, "dmha_reserve: bad args");
   if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_reserve: D=%d", D);
-  const int64_t Lloc = L / world_size;
+  const int64_t Lloc = max_shard_rows(L, world_size, g.layout);
   if (world_size == 1) {
     if (split_kv_active(Lloc, D, H)) return ensure_ring_ws(Lloc, D, H, false, true);
     return DMHA_OK;
@@ -890,8 +920,8 @@ int dmha_reserve(int world_size, int64_t L, int D, int H) {
   if (int rc = ensure_ring_ws(Lloc, D, H, true)) return rc;
   if (g.peer && world_size == g.world) {
     std::string err;
-    const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
-    if (int rc = dmha::peer_ensure_pub(g.peer, 2 * blk, &err)) return fail(rc, "%s", err.c_str());
+    const size_t vo = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+    if (int rc = dmha::peer_ensure_pub(g.peer, 2 * vo, &err)) return fail(rc, "%s", err.c_str());
     update_ws_stat();
   }
   return DMHA_OK;
@@ -920,10 +950,19 @@ int dmha_ring_plan_step(int world_size, int rank, int step, int layout, int64_t 
   if (!plan_out || world_size < 1 || rank < 0 || rank >= world_size || step < 0 ||
       step >= world_size || L < 1)
     return fail(DMHA_ERR_INVALID, "dmha_ring_plan_step: bad args");
-  const int64_t div = layout == DMHA_LAYOUT_ZIGZAG ? 2LL * world_size : world_size;
-  if ((layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG) || L % div)
+  if ((layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG) ||
+      (layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * world_size)))
     return fail(DMHA_ERR_INVALID, "dmha_ring_plan_step: bad layout or L");
   *plan_out = make_plan(world_size, rank, step, layout, L);
+  return DMHA_OK;
+}
+
+int dmha_shard_rows(int64_t L, int world_size, int rank, int layout, int64_t* rows_out) {
+  if (!rows_out || world_size < 1 || rank < 0 || rank >= world_size || L < 1 ||
+      (layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG) ||
+      (layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * world_size)))
+    return fail(DMHA_ERR_INVALID, "dmha_shard_rows: bad args");
+  *rows_out = shard_rows(L, world_size, rank, layout);
   return DMHA_OK;
 }
 
@@ -931,10 +970,11 @@ int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_
                          int64_t* global_out) {
   if (!global_out || world_size < 1 || rank < 0 || rank >= world_size || L < 1)
     return fail(DMHA_ERR_INVALID, "dmha_local_to_global: bad args");
-  const int64_t div = layout == DMHA_LAYOUT_ZIGZAG ? 2LL * world_size : world_size;
-  if ((layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG) || L % div)
+  if ((layout != DMHA_LAYOUT_CONTIGUOUS && layout != DMHA_LAYOUT_ZIGZAG) ||
+      (layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * world_size)))
     return fail(DMHA_ERR_INVALID, "dmha_local_to_global: bad layout or L");
-  if (i < 0 || i >= L / world_size) return fail(DMHA_ERR_INVALID, "dmha_local_to_global: i out of range");
+  if (i < 0 || i >= shard_rows(L, world_size, rank, layout))
+    return fail(DMHA_ERR_INVALID, "dmha_local_to_global: i out of range");
   const dmha::PosMap m = posmap(L, world_size, rank, layout);
   *global_out = i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
   return DMHA_OK;
@@ -951,16 +991,18 @@ int dmha_local_to_global(int64_t L, int world_size, int rank, int layout, int64_
 int peer_forward(const void* q, const void* k, const void* v, void* out, float* lse, int64_t L,
                  int D, int H, int causal) {
   const int P = g.world, r = g.rank;
-  const size_t blk = static_cast<size_t>(L / P) * H * D * elem_bytes(g.dtype);
+  const size_t row_bytes = static_cast<size_t>(H) * D * elem_bytes(g.dtype);
+  const size_t vo = static_cast<size_t>(max_shard_rows(L, P, g.layout)) * row_bytes;  // V offset
+  const size_t blk = static_cast<size_t>(shard_rows(L, P, r, g.layout)) * row_bytes;  // own rows
   std::string err;
-  if (int rc = dmha::peer_ensure_pub(g.peer, 2 * blk, &err)) return fail(rc, "%s", err.c_str());
+  if (int rc = dmha::peer_ensure_pub(g.peer, 2 * vo, &err)) return fail(rc, "%s", err.c_str());
   update_ws_stat();
   if (int rc = dmha::peer_barrier(g.peer, &err)) return fail(rc, "%s", err.c_str());
   for (int p = 0; p < P; ++p)
     if (p != r) CK_CUDA(cudaStreamWaitEvent(g.stream, dmha::peer_done_event(g.peer, p), 0));
   char* pub = static_cast<char*>(dmha::peer_local_pub(g.peer));
   CK_CUDA(cudaMemcpyAsync(pub, k, blk, cudaMemcpyDeviceToDevice, g.stream));
-  CK_CUDA(cudaMemcpyAsync(pub + blk, v, blk, cudaMemcpyDeviceToDevice, g.stream));
+  CK_CUDA(cudaMemcpyAsync(pub + vo, v, blk, cudaMemcpyDeviceToDevice, g.stream));
   CK_CUDA(cudaEventRecord(dmha::peer_pub_event(g.peer, r), g.stream));
   if (int rc = dmha::peer_barrier(g.peer, &err)) return fail(rc, "%s", err.c_str());
   PeerTransport tx(P, r);
@@ -972,7 +1014,9 @@ int peer_forward(const void* q, const void* k, const void* v, void* out, float* 
 int dmha_forward(const void* q, const void* k, const void* v, void* out, float* lse, int64_t L,
                  int D, int H, int causal) {
   if (int rc = check_state()) return rc;
-  if (int rc = validate(q, k, v, out, lse, L, D, H, g.world, g.layout)) return rc;
+  if (int rc = validate(q, k, v, out, lse, L, D, H, g.world, g.layout, 1,
+                        shard_rows(L, g.world, g.rank, g.layout)))
+    return rc;
   if (int rc = poll_nccl()) return rc;
   if (int rc = check_collective_contract(L, D, H, causal)) return rc;
   begin_forward();
@@ -992,8 +1036,9 @@ int dmha_forward_host(const void* q, const void* k, const void* v, void* out, fl
   if (int rc = check_state()) return rc;
   if (!q || !k || !v || !out || !lse) return fail(DMHA_ERR_INVALID, "dmha_forward_host: null pointer");
   begin_forward();
-  if (L < 1 || H < 1 || L % g.world) return fail(DMHA_ERR_INVALID, "dmha_forward_host: bad L/H");
-  const int64_t Lloc = L / g.world;
+  if (L < 1 || H < 1 || (g.layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * g.world)))
+    return fail(DMHA_ERR_INVALID, "dmha_forward_host: bad L/H");
+  const int64_t Lloc = shard_rows(L, g.world, g.rank, g.layout);
   const size_t tb = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
   const size_t lb = static_cast<size_t>(Lloc) * H;
   if (3 * tb > g.st_bytes) {
@@ -1129,20 +1174,23 @@ int dmha_forward_emulated(int world_size, int layout, const void* q, const void*
   if (world_size < 1) return fail(DMHA_ERR_INVALID, "dmha_forward_emulated: world_size < 1");
   if (int rc = validate(q, k, v, out, lse, L, D, H, world_size, layout, world_size)) return rc;
   const int P = world_size;
-  const int64_t Lloc = L / P;
-  const size_t blk = static_cast<size_t>(Lloc) * H * D * elem_bytes(g.dtype);
+  const int64_t Lm = max_shard_rows(L, P, layout);  // rows per shard slot
+  const size_t blk = static_cast<size_t>(Lm) * H * D * elem_bytes(g.dtype);
   begin_forward();
   // Rank r's ring runs through the same loop, buffers, events and streams as
   // dmha_forward at world size P; only the transport differs: each receive is
   // one cudaMemcpyAsync per K / V block on the comm stream from the sending
   // rank's shard.  Ranks run one after the other (no kernel waits on another).
+  // Slot r holds rank r's shard_rows(r) rows first (uneven contiguous shards
+  // leave the last row of a short slot unused); its lse is [H, shard_rows(r)]
+  // packed from the slot start.
   for (int r = 0; r < P; ++r) {
     CopyTransport tx(static_cast<const char*>(k), static_cast<const char*>(v), blk, P, r, layout, L);
     if (int rc = ring_forward(P, r, layout, static_cast<const char*>(q) + r * blk,
                               static_cast<const char*>(k) + r * blk,
                               static_cast<const char*>(v) + r * blk,
                               static_cast<char*>(out) + r * blk,
-                              lse + static_cast<size_t>(r) * Lloc * H, L, D, H, causal ? 1 : 0, tx))
+                              lse + static_cast<size_t>(r) * Lm * H, L, D, H, causal ? 1 : 0, tx))
       return rc;
   }
   g.stats.forwards++;
@@ -1312,10 +1360,10 @@ int dmha_mha_forward(const void* x, const void* wq, const void* wk, const void* 
     return fail(DMHA_ERR_INVALID, "dmha_mha_forward: null pointer");
   if (d_model < 1 || d_model % 8 != 0)
     return fail(DMHA_ERR_INVALID, "dmha_mha_forward: d_model must be a positive multiple of 8");
-  if (L < 1 || H < 1 || L % g.world != 0)
+  if (L < 1 || H < 1 || (g.layout == DMHA_LAYOUT_ZIGZAG && L % (2LL * g.world)))
     return fail(DMHA_ERR_INVALID, "dmha_mha_forward: bad L/H for world size %d", g.world);
   if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_mha_forward: D=%d", D);
-  const int64_t Lloc = L / g.world;
+  const int64_t Lloc = shard_rows(L, g.world, g.rank, g.layout);
   const size_t act = static_cast<size_t>(Lloc) * H * D * 2;
   const size_t lbytes = static_cast<size_t>(Lloc) * H * 4;
   const size_t need = 4 * act + lbytes + 4 * 256;

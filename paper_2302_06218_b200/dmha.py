@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "dmha_get_stats", "dmha_local_to_global", "dmha_attention_local", "dmha_lse_combine",
     "dmha_synchronize", "dmha_set_profiling", "dmha_debug_set_trace", "dmha_ring_plan_step",
     "dmha_forward_headpar", "dmha_forward_headpar_emulated", "dmha_mha_forward", "dmha_linear",
-    "dmha_reserve",
+    "dmha_reserve", "dmha_shard_rows",
     "dmha_select", "dmha_scatter_rows", "dmha_ring_workspace_bytes",
 )
 
@@ -101,6 +101,7 @@ def lib():
             "dmha_mha_forward": [P, P, P, P, P, P, P, I64, I, I, I, I],
             "dmha_linear": [P, P, P, I64, I, I],
             "dmha_reserve": [I, I64, I, I],
+            "dmha_shard_rows": [I64, I, I, I, ctypes.POINTER(I64)],
             "dmha_select": [P, I64, I, I, P, ctypes.c_double, P, P, P, ctypes.POINTER(I64)],
             "dmha_scatter_rows": [P, P, I64, I, P],
         }
@@ -455,13 +456,21 @@ def ring_plan(world_size: int, rank: int, step: int, layout, L: int) -> dict:
     return {f: int(getattr(pl, f)) for f, _ in RingPlan._fields_}
 
 
+def shard_rows(L: int, world_size: int, rank: int, layout) -> int:
+    """Rows rank `rank` owns (dmha_shard_rows: uneven contiguous shards allowed)."""
+    n = ctypes.c_int64(0)
+    _check(lib().dmha_shard_rows(int(L), int(world_size), int(rank), layout_code(layout),
+                                 ctypes.byref(n)))
+    return n.value
+
+
 def global_rows(L: int, world_size: int, rank: int, layout) -> np.ndarray:
     """Global positions of rank `rank`'s local rows, from the library's own
     position map (the q map of dmha_ring_plan_step: two increasing pieces,
     i < chunk -> base0 + i, else base1 + i - chunk; tests check it against
     dmha_local_to_global row by row)."""
     pl = ring_plan(world_size, rank, 0, layout, L)
-    n = L // world_size
+    n = shard_rows(L, world_size, rank, layout)
     c = pl["q_chunk"]
     return np.concatenate([np.arange(pl["q_base0"], pl["q_base0"] + min(c, n)),
                            np.arange(pl["q_base1"], pl["q_base1"] + max(0, n - c))]).astype(np.int64)
@@ -488,14 +497,48 @@ def unshard(parts, L: int, layout):
         if isinstance(first, torch.Tensor):
             outp = torch.empty((L,) + tuple(first.shape[1:]), dtype=first.dtype, device=first.device)
             for r, p in enumerate(parts):
-                outp[torch.from_numpy(global_rows(L, P, r, layout)).to(first.device)] = p
+                idx = global_rows(L, P, r, layout)
+                outp[torch.from_numpy(idx).to(first.device)] = p[:len(idx)]
             return outp
     except ImportError:  # pragma: no cover
         pass
     outp = np.empty((L,) + tuple(first.shape[1:]), dtype=first.dtype)
     for r, p in enumerate(parts):
-        outp[global_rows(L, P, r, layout)] = p
+        idx = global_rows(L, P, r, layout)
+        outp[idx] = p[:len(idx)]  # a padded slot (uneven shards) keeps its rows first
     return outp
+
+
+def stack_shards(x, world_size: int, layout):
+    """Global [L, ...] -> [P, Lm, ...] rank-major shard slots (Lm = the largest
+    shard; short slots zero-padded at the end), the layout dmha_forward_emulated
+    takes."""
+    parts = [shard(x, world_size, r, layout) for r in range(world_size)]
+    Lm = max(len(p) for p in parts)
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            outp = torch.zeros((world_size, Lm) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+            for r, p in enumerate(parts):
+                outp[r, :len(p)] = p
+            return outp
+    except ImportError:  # pragma: no cover
+        pass
+    outp = np.zeros((world_size, Lm) + tuple(x.shape[1:]), dtype=x.dtype)
+    for r, p in enumerate(parts):
+        outp[r, :len(p)] = p
+    return outp
+
+
+def unstack_emulated(out, lse, L: int, layout):
+    """dmha_forward_emulated results -> global out [L, H, D] and lse [H, L]
+    (slot r: its rows first; lse packed as [H, rows] from the slot start)."""
+    P, Lm, H = out.shape[0], out.shape[1], out.shape[2]
+    rows = [shard_rows(L, P, r, layout) for r in range(P)]
+    o_parts = [out[r][:rows[r]] for r in range(P)]
+    flat = lse.reshape(P, -1)
+    l_parts = [flat[r][:H * rows[r]].reshape(H, rows[r]).T for r in range(P)]
+    return unshard(o_parts, L, layout), unshard(l_parts, L, layout).T
 
 
 def attention_flops(L: int, D: int, H: int, causal: bool) -> float:

@@ -94,9 +94,25 @@ def test_shard_unshard_roundtrip():
         np.testing.assert_array_equal(dmha.unshard(parts, 48, layout), x)
 
 
-def test_bad_layout_args():
+def test_uneven_contiguous_shards_follow_spec_example():
+    """SPEC S:445's equal-as-possible partition: L = 10 over 4 workers is
+    {3, 3, 2, 2} rows, in order (rank r starts at r*(L/P) + min(r, L % P))."""
+    assert [dmha.shard_rows(10, 4, r, "contiguous") for r in range(4)] == [3, 3, 2, 2]
+    rows = [list(dmha.global_rows(10, 4, r, "contiguous")) for r in range(4)]
+    assert rows == [[0, 1, 2], [3, 4, 5], [6, 7], [8, 9]]
+    assert [dmha.local_to_global(10, 4, 2, "contiguous", i) for i in range(2)] == [6, 7]
     with pytest.raises(dmha.DmhaError):
-        dmha.local_to_global(10, 4, 0, "contiguous", 0)   # 10 % 4 != 0
+        dmha.local_to_global(10, 4, 2, "contiguous", 2)   # rank 2 owns 2 rows
+    # every L and P: the shards partition [0, L) in order, sizes differ by <= 1
+    for L in range(1, 40):
+        for P in range(1, 9):
+            g = np.concatenate([dmha.global_rows(L, P, r, "contiguous") for r in range(P)])
+            assert np.array_equal(g, np.arange(L))
+            sz = [dmha.shard_rows(L, P, r, "contiguous") for r in range(P)]
+            assert max(sz) - min(sz) <= 1
+
+
+def test_bad_layout_args():
     with pytest.raises(dmha.DmhaError):
         dmha.local_to_global(12, 4, 0, "zigzag", 0)       # 12 % 8 != 0
     with pytest.raises(dmha.DmhaError):

@@ -577,3 +577,27 @@ def test_forward_captures_into_cuda_graph(lib_bf16, case):
         fwd()
         torch.cuda.synchronize()
         assert torch.equal(g_o, out) and torch.equal(g_l, lse), f"{case} seed {seed}"
+
+
+@pytest.mark.parametrize("P,extra,causal,D", [(3, 1, False, 64), (4, 3, True, 128), (5, 2, True, 64),
+                                               (8, 5, False, 128), (2, 1, True, 64)])
+def test_emulated_ring_uneven_shards(lib_bf16, oracle_mod, P, extra, causal, D):
+    """Uneven contiguous shards (L % P != 0; SPEC S:438-446 equal-as-possible:
+    the first L % P ranks hold one row more): the ring moves each block at its
+    owner's size, ragged query/key tiles and global-position masks — against
+    the oracle, and the exact per-forward byte count."""
+    L, H = 300 * P + extra, 2
+    q, k, v = inputs.qkv(L, H, D, seed=1900 + P + extra)
+    parts = [dmha.stack_shards(x, P, "contiguous") for x in (q, k, v)]
+    dmha.get_stats()
+    out, lse = dmha.forward_emulated(P, "contiguous", *(to_dev(x) for x in parts), L, causal)
+    torch.cuda.synchronize()
+    og, lg = dmha.unstack_emulated(out.float().cpu().numpy(), lse.cpu().numpy(), L, "contiguous")
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(og, lg, ref_o, ref_l, "bf16", f"uneven ring P={P} L={L} causal={causal} D={D}")
+    rows = [dmha.shard_rows(L, P, r, "contiguous") for r in range(P)]
+    assert sorted(set(rows)) == sorted({L // P, L // P + 1})
+    # the emulation sums every rank's sends: (P-1) blocks per rank, each block
+    # sized by its owner
+    sent = sum(rows[(r - s) % P] for r in range(P) for s in range(P - 1)) * H * D * 2 * 2
+    assert dmha.get_stats()["last_bytes_sent"] == sent

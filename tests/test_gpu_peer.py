@@ -63,10 +63,14 @@ def _run_ranks(P, L, H, D, causal, layout, nfwd=3):
     return res
 
 
-@pytest.mark.parametrize("P,layout,causal,D", [(2, "contiguous", False, 128), (2, "zigzag", True, 64),
-                                               (3, "contiguous", True, 64), (4, "zigzag", True, 128)])
-def test_peer_transport_processes(oracle_mod, P, layout, causal, D):
-    L, H = 256 * P * 2 + (0 if layout == "zigzag" else 64 * P), 2
+@pytest.mark.parametrize("P,layout,causal,D,extra", [(2, "contiguous", False, 128, 0),
+                                                     (2, "zigzag", True, 64, 0),
+                                                     (3, "contiguous", True, 64, 0),
+                                                     (4, "zigzag", True, 128, 0),
+                                                     (3, "contiguous", True, 128, 2)])
+def test_peer_transport_processes(oracle_mod, P, layout, causal, D, extra):
+    """extra > 0: uneven contiguous shards (L % P == extra)."""
+    L, H = 256 * P * 2 + (0 if layout == "zigzag" else 64 * P) + extra, 2
     if layout == "zigzag":
         L -= L % (2 * P)
     res = _run_ranks(P, L, H, D, causal, layout)
@@ -74,19 +78,21 @@ def test_peer_transport_processes(oracle_mod, P, layout, causal, D):
     # reference 1: the single-GPU emulation of the same ring (bit-identical)
     dmha.init(1, 0, None, 0, "bf16", layout)
     try:
-        parts = [np.stack([dmha.shard(x, P, r, layout) for r in range(P)]) for x in (q, k, v)]
+        parts = [dmha.stack_shards(x, P, layout) for x in (q, k, v)]
         dq, dk, dv = (torch.from_numpy(x).cuda().to(torch.bfloat16) for x in parts)
         eo, el = dmha.forward_emulated(P, layout, dq, dk, dv, L, causal)
         torch.cuda.synchronize()
-        eo, el = eo.float().cpu().numpy(), el.cpu().numpy()
+        eo, el = eo.float().cpu().numpy(), el.cpu().numpy().reshape(P, -1)
+        rows = [dmha.shard_rows(L, P, r, layout) for r in range(P)]
     finally:
         dmha.finalize()
     for r in range(P):
-        np.testing.assert_array_equal(res[r][0], eo[r])
-        np.testing.assert_array_equal(res[r][1], el[r])
-        # exact accounting: P-1 pulls of one K and one V block per forward
-        blk = (L // P) * H * D * 2
-        assert int(res[r][2][0]) == (P - 1) * 2 * blk and int(res[r][2][1]) == P - 1
+        np.testing.assert_array_equal(res[r][0], eo[r][:rows[r]])
+        np.testing.assert_array_equal(res[r][1], el[r][:H * rows[r]].reshape(H, rows[r]))
+        # exact accounting: P-1 sends, each of the block the rank holds at that
+        # step (its owner's rows x H x D bf16, K and V)
+        sent = sum(rows[(r - s) % P] for s in range(P - 1)) * H * D * 2 * 2
+        assert int(res[r][2][0]) == sent and int(res[r][2][1]) == P - 1
     # reference 2: the fp64 oracle
     out = dmha.unshard([res[r][0] for r in range(P)], L, layout)
     lse = dmha.unshard([res[r][1].T for r in range(P)], L, layout).T

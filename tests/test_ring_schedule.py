@@ -45,7 +45,8 @@ def _worker(rank, world, port, L, H, D, layout, causal, out_dir):
 
     q, k, v = inputs.qkv(L, H, D, seed=4242)
     my_rows = dmha.global_rows(L, world, rank, layout)
-    Lloc = L // world
+    Lloc = len(my_rows)  # uneven contiguous shards: L/P or L/P + 1 rows
+    assert Lloc == dmha.shard_rows(L, world, rank, layout)
     kv_cur = np.concatenate([k[my_rows], v[my_rows]]).astype(np.float32)  # step 0: own block
     ring = [None, None]
     o_acc = lse_acc = None
@@ -53,14 +54,17 @@ def _worker(rank, world, port, L, H, D, layout, causal, out_dir):
         pl = dmha.ring_plan(world, rank, s, layout, L)
         q_glob = _rows_of(pl["q_base0"], pl["q_base1"], pl["q_chunk"], Lloc)
         assert np.array_equal(q_glob, my_rows)
-        k_glob = _rows_of(pl["k_base0"], pl["k_base1"], pl["k_chunk"], Lloc)
+        nk = dmha.shard_rows(L, world, pl["src"], layout)  # the block's owner's rows
+        k_glob = _rows_of(pl["k_base0"], pl["k_base1"], pl["k_chunk"], nk)
         assert np.array_equal(k_glob, dmha.global_rows(L, world, pl["src"], layout))
         kv_use = kv_cur if pl["compute_buf"] < 0 else ring[pl["compute_buf"]]
         # the block really is the src rank's keys (data arrived through the ring)
-        np.testing.assert_array_equal(kv_use[:Lloc], k[k_glob])
-        # exchange for the next step (send current block, receive the next)
+        np.testing.assert_array_equal(kv_use[:nk], k[k_glob])
+        # exchange for the next step (send current block, receive the next,
+        # sized by ITS owner's rows)
         if pl["recv_buf"] >= 0:
-            recv = torch.empty(2 * Lloc, H, D)
+            nxt = dmha.ring_plan(world, rank, s + 1, layout, L)["src"]
+            recv = torch.empty(2 * dmha.shard_rows(L, world, nxt, layout), H, D)
             reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(kv_use)), pl["send_to"]),
                     dist.irecv(recv, pl["recv_from"])]
             for r_ in reqs:
@@ -70,8 +74,8 @@ def _worker(rank, world, port, L, H, D, layout, causal, out_dir):
         # partial over this block's keys at global positions (oracle on a gathered view)
         kk = np.zeros((L, H, D), np.float32)
         vv = np.zeros((L, H, D), np.float32)
-        kk[k_glob] = kv_use[:Lloc]
-        vv[k_glob] = kv_use[Lloc:]
+        kk[k_glob] = kv_use[:nk]
+        vv[k_glob] = kv_use[nk:]
         mask_keys = np.zeros(L, bool)
         mask_keys[k_glob] = True
         # contiguous key ranges of the block (one or two chunks)
@@ -117,10 +121,12 @@ def _merge_list(parts):
     return o, l
 
 
-@pytest.mark.parametrize("world,layout,causal", [(2, "contiguous", False), (2, "zigzag", True),
-                                                  (4, "zigzag", True), (4, "contiguous", True)])
-def test_ring_over_gloo_matches_oracle(tmp_path, oracle_mod, world, layout, causal):
-    L, H, D = 96 * world, 2, 8
+@pytest.mark.parametrize("world,layout,causal,extra", [(2, "contiguous", False, 0), (2, "zigzag", True, 0),
+                                                        (4, "zigzag", True, 0), (4, "contiguous", True, 0),
+                                                        (4, "contiguous", True, 3), (3, "contiguous", False, 1)])
+def test_ring_over_gloo_matches_oracle(tmp_path, oracle_mod, world, layout, causal, extra):
+    """extra > 0: L % P == extra, uneven contiguous shards."""
+    L, H, D = 96 * world + extra, 2, 8
     port = _free_port()
     mp.spawn(_worker, args=(world, port, L, H, D, layout, causal, str(tmp_path)), nprocs=world, join=True)
     from paper_2302_06218_b200 import dmha
