@@ -50,6 +50,8 @@ WORKLOADS = {
                 desc="C5-shaped A/B workload L=131072 D=64 H=16 bf16 causal"),
     "C5nc": dict(L=131072, D=64, H=16, causal=False, dtype="bf16", layout="contiguous",
                  desc="A/B workload L=131072 D=64 H=16 bf16 non-causal"),
+    "C2f": dict(L=16384, D=64, H=8, causal=False, dtype="fp32", layout="contiguous",
+                desc="A/B workload L=16384 D=64 H=8 fp32 non-causal (C2's shape on the fp32 path)"),
     "C2x4": dict(L=65536, D=64, H=8, causal=False, dtype="bf16", layout="contiguous",
                  desc="A/B workload L=65536 D=64 H=8 bf16 non-causal (C2 heads, 4x longer)"),
 }

@@ -112,9 +112,18 @@ __global__ void __launch_bounds__(256) attn_fwd_fp32_kernel(const float* __restr
 
 }  // namespace
 
-cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream) {
+static bool fp32_simt() {
   const char* e = std::getenv("DMHA_FP32_SIMT");
-  if (!(e && std::atoi(e) != 0)) return launch_attn_fwd_tf32x3(a, stream);
+  return e && std::atoi(e) != 0;
+}
+
+int fp32_launches_per_call(int64_t Lq, int64_t Lk) {
+  if (Lq <= 0) return 0;
+  return fp32_simt() ? 1 : (Lk > 0 ? 2 : 1);
+}
+
+cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream) {
+  if (!fp32_simt()) return launch_attn_fwd_tf32x3(a, stream);
   if (a.Lq <= 0) return cudaSuccess;
   const int64_t warps = a.Lq * a.H;
   const int64_t blocks = (warps * 32 + 255) / 256;

@@ -2,24 +2,30 @@
 // L=512, D=64, H=4, fp32, rel L2 <= 1e-4) on the tcgen05 tensor cores with
 // 3xTF32 split arithmetic for BOTH contractions (SURVEY §8(c) reading 13,
 // DESIGN.md R13: one-pass TF32 misses 1e-4, 3xTF32 on QK^T and PV passes):
-//   x = hi + lo,  hi = tf32_rna(x),  lo = x - hi          (exact in fp32)
+//   x = hi + lo,  hi = x rounded to tf32 (nearest, ties away),  lo = x - hi
 //   S  = Qlo Khi^T + Qhi Klo^T + Qhi Khi^T
 //   O += Plo Vhi   + Phi Vlo   + Phi Vhi
 // (small terms first; lo*lo is below fp32 rounding), accumulated in fp32 in
 // TMEM.  The row softmax runs in fp32 with the same
-// global-position causal rule and 1/sqrt(D) scale as the bf16 kernel, and P is
-// split hi/lo the same way before the PV product.
+// global-position causal rule, 1/sqrt(D) scale and lazy rescale rule as the
+// bf16 kernel.
 //
-// CTA = one 128-row query tile of one head, 4 warps (thread t <-> TMEM lane t
-// <-> query row t).  Per 64-key (D = 64) / 32-key (D = 128) tile: all threads
-// load K and V from global memory (coalesced 16-byte loads), split them and
-// store hi / lo into shared memory in the 128-byte-swizzled K-major layout the
-// tcgen05 descriptors read (V transposed, so both operands are K-major); one
-// thread issues the three QK^T products; the softmax threads read S from TMEM,
-// rescale O when the running max grows, write P hi / lo to shared memory; one
-// thread issues the three PV products.  The steps are not overlapped: C1 is
-// 512 x 512 x 4 heads (latency-bound), and the kernel exists for exactness on
-// the tensor cores, not for the bf16 path's throughput.
+// Two launches per local attention call:
+//  1. tf32_split_kv_kernel: K -> K hi / lo ([Lk, H, D]) and V -> V^T hi / lo
+//     ([H, D, Lk4], keys contiguous) in the caller's scratch (the tf32 MMA
+//     reads both operands K-major, so V is transposed once here instead of in
+//     every CTA).
+//  2. attn_fwd_tf32x3_kernel: CTA = one 128-row query tile of one head,
+//     8 warps:
+//       warp 0     TMA producer of K hi / lo     (kKST-slot ring)
+//       warp 1     TMEM allocator + MMA issuer
+//       warp 2     TMA producer of V^T hi / lo   (kVST-slot ring)
+//       warps 4-7  softmax + epilogue (thread <-> TMEM lane <-> query row)
+//     Both A operands live in TMEM (Q hi / lo written once by the softmax
+//     threads; P hi over the S columns it came from, P lo in its own
+//     columns), so the tensor core reads only the K / V^T tiles from shared
+//     memory.  S and P are double-buffered: the issuer runs QK^T one tile
+//     ahead of PV, and softmax(j) overlaps PV(j-1) + QK^T(j+1).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -28,53 +34,76 @@
 
 #include "kernels.h"
 #include "ptx_sm100.cuh"
+#include "tma_map.h"
 
-// TF32_WAIT: the kernel's mbarrier wait (tools/tf32_kernel_probe.cu
-// redefines it as a bounded wait that reports where a CTA stalls).
+// TF32_WAIT: the kernel's mbarrier wait (a probe build can redefine it as a
+// bounded wait that reports where a CTA stalls).
+// -DDMHA_TF32_BOUNDED=1 (debug build): give up after ~2^28 polls, print the
+// tag (which wait, which tile) and trap, so a protocol bug is an error, not
+// a hung GPU.
 #ifndef TF32_WAIT
+#if DMHA_TF32_BOUNDED
+#include <cstdio>
+#define TF32_WAIT(bar, phase, tag)                                                         \
+  do {                                                                                     \
+    uint32_t n_ = 0;                                                                       \
+    while (!ptx::mbar_try_wait(bar, phase)) {                                              \
+      if (++n_ == (1u << 28)) {                                                            \
+        printf("tf32 wait timeout tag %d block (%d,%d) thread %d\n", (tag), blockIdx.x,     \
+               blockIdx.y, threadIdx.x);                                                   \
+        __trap();                                                                          \
+      }                                                                                    \
+    }                                                                                      \
+  } while (0)
+#else
 #define TF32_WAIT(bar, phase, tag) ptx::mbar_wait(bar, phase)
+#endif
+#endif
+
+// Tiles per TMEM accumulation chunk of O (measurement knob; see kFlush).
+#ifndef DMHA_TF32_FLUSH
+#define DMHA_TF32_FLUSH 4
 #endif
 
 namespace dmha {
 namespace {
 
 constexpr int kBM = 128;
+constexpr float kTf32RescaleThreshold = 8.0f;  // log2 units, as the bf16 kernel
 
 template <int D>
 struct Tf32Cfg {
-  static constexpr int kBN = D == 64 ? 64 : 32;      // keys per tile
-  static constexpr int kQBytes = kBM * D * 4;         // one of Q hi / lo
-  static constexpr int kKBytes = kBN * D * 4;         // one of K hi / lo
-  static constexpr int kVBytes = D * kBN * 4;         // one of V^T hi / lo
-  static constexpr int kPBytes = kBM * kBN * 4;       // one of P hi / lo
-  static constexpr int kQh = 0, kQl = kQh + kQBytes;
-  static constexpr int kKh = kQl + kQBytes, kKl = kKh + kKBytes;
-  static constexpr int kVh = kKl + kKBytes, kVl = kVh + kVBytes;
-  static constexpr int kPh = kVl + kVBytes, kPl = kPh + kPBytes;
-  static constexpr int kBar = kPl + kPBytes;
-  static constexpr int kSmem = kBar + 64 + 1024;
+  static constexpr int kBN = D == 64 ? 64 : 32;  // keys per tile
+  static constexpr int kKST = 3, kVST = 2;        // ring slots
+  static constexpr int kKOp = kBN * D * 4;        // one of K hi / lo
+  static constexpr int kVOp = D * kBN * 4;        // one of V^T hi / lo
+  static constexpr int kKOff = 0;
+  static constexpr int kVOff = kKOff + kKST * 2 * kKOp;
+  // fp32 master copy of O (one 128-row tile; 16-byte chunks XOR-swizzled by
+  // row so a warp's row-per-thread accesses are conflict-free)
+  static constexpr int kMOff = kVOff + kVST * 2 * kVOp;
+  static constexpr int kBarOff = kMOff + kBM * D * 4;
+  // PV restarts its TMEM accumulator every kFlush tiles after the softmax
+  // threads have added the partial into the master copy (see the kernel)
+  static constexpr int kFlush = DMHA_TF32_FLUSH;
+  // kfull[KST] kempty[KST] vfull[VST] vempty[VST] sfull[2] pready[2] oready
+  // ofinal qready
+  static constexpr int kNumBars = 2 * kKST + 2 * kVST + 7;
+  static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
+  // TMEM columns (fp32 / tf32: one element per column)
+  static constexpr int cQh = 0, cQl = D, cS = 2 * D, cPl = cS + 2 * kBN, cO = cPl + 2 * kBN;
   static constexpr uint32_t kIdescS = ptx::make_idesc(2, kBM, kBN, 0, 0);  // tf32, K-major
   static constexpr uint32_t kIdescO = ptx::make_idesc(2, kBM, D, 0, 0);
-  static constexpr int kTmemS = 0, kTmemO = 128;  // S: kBN columns, O: D columns
+  static_assert(cO + D <= 512, "TMEM budget");
   static_assert(kSmem <= 232448, "shared memory budget");
+  static_assert(kBN % 32 == 0 && D % 32 == 0, "32-column TMEM chunks");
 };
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-// Byte offset of 16-byte chunk c (4 fp32 along K) of row `row` in a K-major
-// operand of `rows` rows, 128-byte swizzle: 32 fp32 of K per 128-byte panel
-// row, panels of rows x 128 B, chunk index XOR (row % 8).
-__device__ __forceinline__ uint32_t sw_off(int rows, int row, int c) {
-  return static_cast<uint32_t>((c >> 3) * rows * 128 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
-}
-
-__device__ __forceinline__ void split4(float4 x, float4& hi, float4& lo) {
-  hi = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-  lo = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+// x = hi + lo with hi = x rounded to tf32 (10 mantissa bits, nearest, ties
+// away from zero on the magnitude) and lo = x - hi exact in fp32.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  lo = x - hi;
 }
 
 __device__ __forceinline__ int64_t pos_tf(const PosMap& m, int64_t i) {
@@ -96,212 +125,414 @@ __device__ __forceinline__ int64_t klimit_tf(int causal, const PosMap& km, int64
   return lim < Lk ? lim : Lk;
 }
 
-// D[tmem] (+)= A * B^T over K = kdim (K-major tf32 operands of ra / rb rows)
-__device__ __forceinline__ void mma_tf32_kloop(uint32_t d, uint32_t a, int ra, uint32_t b, int rb,
+// D[tmem] (+)= A[tmem] * B[smem desc]  (kind::tf32, A read from tensor memory)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// D (+)= A * B^T over K = kdim: A = kdim TMEM columns from a_col, B = a
+// K-major 128-byte-swizzled shared-memory operand of b_rows rows (panels of
+// 32 fp32 along K).  Eight K elements per instruction.
+__device__ __forceinline__ void mma_tf32_kloop(uint32_t d, uint32_t a_col, uint32_t b, int b_rows,
                                                int kdim, uint32_t idesc, bool acc) {
   for (int kk = 0; kk < kdim / 8; ++kk) {
-    const uint32_t off_a = (kk >> 2) * ra * 128 + (kk & 3) * 32;
-    const uint32_t off_b = (kk >> 2) * rb * 128 + (kk & 3) * 32;
-    ptx::mma_tf32_ss(d, ptx::smem_desc_sw128(a + off_a, 16, 1024),
-                     ptx::smem_desc_sw128(b + off_b, 16, 1024), idesc, (acc || kk > 0) ? 1u : 0u);
+    const uint32_t off = (kk >> 2) * b_rows * 128 + (kk & 3) * 32;
+    mma_tf32_ts(d, a_col + kk * 8, ptx::smem_desc_sw128(b + off, 16, 1024), idesc,
+                (acc || kk > 0) ? 1u : 0u);
   }
 }
 
+// ---------------------------------------------------------------- launch 1
+// Block = 32 keys of one head: K split elementwise (coalesced along D), V
+// split and transposed through shared memory (one 128-byte row of 32 keys
+// per warp store).  Keys in [Lk, Lk4) of V^T are written as zeros.
 template <int D>
-__global__ void __launch_bounds__(128, 1)
-    attn_fwd_tf32x3_kernel(const float* __restrict__ q, const float* __restrict__ k,
-                           const float* __restrict__ v, float* __restrict__ out,
-                           float* __restrict__ lse, int64_t Lq, int64_t Lk, int H, int causal,
-                           PosMap qmap, PosMap kmap, float scale_log2) {
+__global__ void __launch_bounds__(256) tf32_split_kv_kernel(
+    const float* __restrict__ k, const float* __restrict__ v, float* __restrict__ kh,
+    float* __restrict__ kl, float* __restrict__ vth, float* __restrict__ vtl, int64_t Lk,
+    int64_t Lk4, int H) {
+  __shared__ float tile[32][D + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int head = blockIdx.y;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 32;
+  for (int i = tid; i < 32 * (D / 4); i += 256) {
+    const int r = i / (D / 4), c = i % (D / 4);
+    const int64_t key = j0 + r;
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (key < Lk) {
+      const int64_t e4 = (key * H + head) * (D / 4) + c;
+      const float4 x = reinterpret_cast<const float4*>(k)[e4];
+      float4 h, l;
+      split_tf32(x.x, h.x, l.x);
+      split_tf32(x.y, h.y, l.y);
+      split_tf32(x.z, h.z, l.z);
+      split_tf32(x.w, h.w, l.w);
+      reinterpret_cast<float4*>(kh)[e4] = h;
+      reinterpret_cast<float4*>(kl)[e4] = l;
+      y = reinterpret_cast<const float4*>(v)[e4];
+    }
+    tile[r][4 * c] = y.x;
+    tile[r][4 * c + 1] = y.y;
+    tile[r][4 * c + 2] = y.z;
+    tile[r][4 * c + 3] = y.w;
+  }
+  __syncthreads();
+  const int64_t key = j0 + lane;
+  if (key >= Lk4) return;
+  for (int d = warp; d < D; d += 8) {
+    float h, l;
+    split_tf32(tile[lane][d], h, l);
+    const int64_t o = (static_cast<int64_t>(head) * D + d) * Lk4 + key;
+    vth[o] = h;
+    vtl[o] = l;
+  }
+}
+
+// ---------------------------------------------------------------- launch 2
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tf32x3_kernel(const __grid_constant__ CUtensorMap tm_kh,
+                           const __grid_constant__ CUtensorMap tm_kl,
+                           const __grid_constant__ CUtensorMap tm_vh,
+                           const __grid_constant__ CUtensorMap tm_vl, const float* __restrict__ q,
+                           float* __restrict__ out, float* __restrict__ lse, int64_t Lq,
+                           int64_t Lk, int H, int causal, PosMap qmap, PosMap kmap,
+                           float scale_log2) {
   using C = Tf32Cfg<D>;
-  constexpr int kBN = C::kBN;
+  constexpr int kBN = C::kBN, kKST = C::kKST, kVST = C::kVST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::kBar);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
-  const int tid = threadIdx.x;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::kBarOff);
+  uint64_t* kfull = bars;
+  uint64_t* kempty = kfull + kKST;
+  uint64_t* vfull = kempty + kKST;
+  uint64_t* vempty = vfull + kVST;
+  uint64_t* sfull = vempty + kVST;
+  uint64_t* pready = sfull + 2;
+  uint64_t* oready = pready + 2;
+  uint64_t* ofinal = oready + 1;
+  uint64_t* qready = ofinal + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qready + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int head = blockIdx.y;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
+  // tiles this CTA visits: the key prefix its last row may use
+  const int64_t last = (m0 + kBM - 1 < Lq - 1) ? m0 + kBM - 1 : Lq - 1;
+  const int64_t kmax = klimit_tf(causal, kmap, Lk, pos_tf(qmap, last));
+  const int ntiles = static_cast<int>((kmax + kBN - 1) / kBN);
 
   if (tid == 0) {
-    ptx::mbar_init(bar, 1);
+    for (int i = 0; i < kKST; ++i) {
+      ptx::mbar_init(&kfull[i], 1);
+      ptx::mbar_init(&kempty[i], 1);
+    }
+    for (int i = 0; i < kVST; ++i) {
+      ptx::mbar_init(&vfull[i], 1);
+      ptx::mbar_init(&vempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&sfull[i], 1);
+      ptx::mbar_init(&pready[i], 128);
+    }
+    ptx::mbar_init(oready, 1);
+    ptx::mbar_init(ofinal, 1);
+    ptx::mbar_init(qready, 128);
     ptx::fence_mbar_init();
   }
-  if (tid < 32) ptx::tmem_alloc<256>(tmem_slot);
-  // Q tile -> hi / lo (rows past Lq are zero)
-  for (int i = tid; i < kBM * (D / 4); i += 128) {
-    const int r = i / (D / 4), c = i % (D / 4);
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (m0 + r < Lq) x = reinterpret_cast<const float4*>(q + ((m0 + r) * H + head) * D)[c];
-    float4 hi, lo;
-    split4(x, hi, lo);
-    *reinterpret_cast<float4*>(sm + C::kQh + sw_off(kBM, r, c)) = hi;
-    *reinterpret_cast<float4*>(sm + C::kQl + sw_off(kBM, r, c)) = lo;
-  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = ptx::smem_u32(sm);
 
-  const int64_t row = m0 + tid;
-  const bool row_ok = row < Lq;
-  const int64_t qp = pos_tf(qmap, row_ok ? row : Lq - 1);
-  const int64_t klim = klimit_tf(causal, kmap, Lk, qp);
-  // tiles this CTA visits: the prefix its last row may use
-  const int64_t last = (m0 + kBM - 1 < Lq - 1) ? m0 + kBM - 1 : Lq - 1;
-  const int64_t kmax = klimit_tf(causal, kmap, Lk, pos_tf(qmap, last));
-  const int ntiles = static_cast<int>((kmax + kBN - 1) / kBN);
-  const uint32_t lane_addr = static_cast<uint32_t>((tid & ~31) << 16);
-  const uint32_t tS = tmem + lane_addr + C::kTmemS;
-  const uint32_t tO = tmem + lane_addr + C::kTmemO;
-
-  float m_run = -INFINITY, l_run = 0.f;
-  uint32_t phase = 0;
-  for (int jt = 0; jt < ntiles; ++jt) {
-    const int64_t j0 = static_cast<int64_t>(jt) * kBN;
-    // K_j, V_j -> hi / lo (keys past Lk are zero; they are masked below)
-    for (int i = tid; i < kBN * (D / 4); i += 128) {
-      const int r = i / (D / 4), c = i % (D / 4);
-      float4 kx = make_float4(0.f, 0.f, 0.f, 0.f), vx = kx;
-      if (j0 + r < Lk) {
-        kx = reinterpret_cast<const float4*>(k + ((j0 + r) * H + head) * D)[c];
-        vx = reinterpret_cast<const float4*>(v + ((j0 + r) * H + head) * D)[c];
-      }
-      float4 hi, lo;
-      split4(kx, hi, lo);
-      *reinterpret_cast<float4*>(sm + C::kKh + sw_off(kBN, r, c)) = hi;
-      *reinterpret_cast<float4*>(sm + C::kKl + sw_off(kBN, r, c)) = lo;
-      // V^T: row d, K index = key r (element (d, r) of a D-row operand)
-      split4(vx, hi, lo);
-      const float hs[4] = {hi.x, hi.y, hi.z, hi.w}, ls[4] = {lo.x, lo.y, lo.z, lo.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int d = 4 * c + e;
-        const uint32_t o = sw_off(D, d, r >> 2) + (r & 3) * 4;
-        *reinterpret_cast<float*>(sm + C::kVh + o) = hs[e];
-        *reinterpret_cast<float*>(sm + C::kVl + o) = ls[e];
-      }
+  if (warp == 0) {
+    // ---- K hi / lo producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tm_kh);
+      ptx::tma_prefetch_desc(&tm_kl);
     }
-    ptx::fence_proxy_async_smem();
-    ptx::tc_fence_before();
-    __syncthreads();
-    // one thread issues; the rest of its warp waits at __syncwarp (not in the
-    // mbarrier spin below, which could starve the issuing lane)
-    if (tid < 32) {
-      if (tid == 0) {
-        ptx::tc_fence_after();
-        const uint32_t d = tmem + C::kTmemS;
-        mma_tf32_kloop(d, sbase + C::kQl, kBM, sbase + C::kKh, kBN, D, C::kIdescS, false);
-        mma_tf32_kloop(d, sbase + C::kQh, kBM, sbase + C::kKl, kBN, D, C::kIdescS, true);
-        mma_tf32_kloop(d, sbase + C::kQh, kBM, sbase + C::kKh, kBN, D, C::kIdescS, true);
-        ptx::mma_commit(bar);
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j % kKST;
+      if (j >= kKST) TF32_WAIT(&kempty[st], ((j / kKST) - 1) & 1, 100);
+      if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(&kfull[st], 2 * C::kKOp);
+        uint8_t* dst = sm + C::kKOff + st * 2 * C::kKOp;
+#pragma unroll
+        for (int p = 0; p < D / 32; ++p) {
+          ptx::tma_load_3d(&tm_kh, &kfull[st], dst + p * kBN * 128, p * 32, head, j * kBN);
+          ptx::tma_load_3d(&tm_kl, &kfull[st], dst + C::kKOp + p * kBN * 128, p * 32, head,
+                           j * kBN);
+        }
       }
       __syncwarp();
     }
-    TF32_WAIT(bar, phase, 1000 + jt);
-    phase ^= 1;
-    ptx::tc_fence_after();
-    // ---- online softmax of this row (fp32, exp2 domain)
-    float s[kBN];
-#pragma unroll
-    for (int c = 0; c < kBN / 32; ++c)
-      ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<float(*)[32]>(&s[32 * c]));
-    ptx::tmem_wait_ld();
-    const int64_t nv = klim - j0;
-    float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < kBN; ++c) {
-      s[c] = (c < nv) ? s[c] * scale_log2 : -INFINITY;
-      mx = fmaxf(mx, s[c]);
+  } else if (warp == 2) {
+    // ---- V^T hi / lo producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tm_vh);
+      ptx::tma_prefetch_desc(&tm_vl);
     }
-    const float m_new = fmaxf(m_run, mx);
-    const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-    const float alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_use);
-    float sum = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j % kVST;
+      if (j >= kVST) TF32_WAIT(&vempty[st], ((j / kVST) - 1) & 1, 200);
+      if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(&vfull[st], 2 * C::kVOp);
+        uint8_t* dst = sm + C::kVOff + st * 2 * C::kVOp;
 #pragma unroll
-    for (int c = 0; c < kBN; c += 4) {
-      float4 pv, hi, lo;
-      pv.x = exp2f(s[c] - m_use);
-      pv.y = exp2f(s[c + 1] - m_use);
-      pv.z = exp2f(s[c + 2] - m_use);
-      pv.w = exp2f(s[c + 3] - m_use);
-      sum += (pv.x + pv.y) + (pv.z + pv.w);
-      split4(pv, hi, lo);
-      *reinterpret_cast<float4*>(sm + C::kPh + sw_off(kBM, tid, c >> 2)) = hi;
-      *reinterpret_cast<float4*>(sm + C::kPl + sw_off(kBM, tid, c >> 2)) = lo;
+        for (int p = 0; p < kBN / 32; ++p) {
+          ptx::tma_load_3d(&tm_vh, &vfull[st], dst + p * D * 128, j * kBN + p * 32, 0, head);
+          ptx::tma_load_3d(&tm_vl, &vfull[st], dst + C::kVOp + p * D * 128, j * kBN + p * 32, 0,
+                           head);
+        }
+      }
+      __syncwarp();
     }
-    l_run = l_run * alpha + sum;
-    // O (complete: the previous PV was waited for) *= alpha.  tcgen05.ld/st are
-    // warp-collective (.sync.aligned): the whole warp takes the branch when any
-    // of its rows needs it (alpha = 1 for the others).
-    if (__any_sync(0xffffffffu, jt > 0 && m_new > m_run)) {
+  } else if (warp == 1) {
+    // ---- MMA issuer: QK(0), QK(1), then PV(j), QK(j+2) ...  One lane
+    // issues; the warp waits on the barriers together (no lane spins alone).
+    auto issue_qk = [&](int j) {
+      const int st = j % kKST;
+      TF32_WAIT(&kfull[st], (j / kKST) & 1, 300);
+      ptx::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t d = tmem + C::cS + (j & 1) * kBN;
+        const uint32_t kh = sbase + C::kKOff + st * 2 * C::kKOp, kl = kh + C::kKOp;
+        mma_tf32_kloop(d, tmem + C::cQl, kh, kBN, D, C::kIdescS, false);
+        mma_tf32_kloop(d, tmem + C::cQh, kl, kBN, D, C::kIdescS, true);
+        mma_tf32_kloop(d, tmem + C::cQh, kh, kBN, D, C::kIdescS, true);
+        ptx::mma_commit(&kempty[st]);
+        ptx::mma_commit(&sfull[j & 1]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int j) {
+      const int b = j & 1, st = j % kVST;
+      TF32_WAIT(&pready[b], (j >> 1) & 1, 400);
+      TF32_WAIT(&vfull[st], (j / kVST) & 1, 500);
+      ptx::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t d = tmem + C::cO;
+        const uint32_t vh = sbase + C::kVOff + st * 2 * C::kVOp, vl = vh + C::kVOp;
+        const uint32_t ph = tmem + C::cS + b * kBN, pl = tmem + C::cPl + b * kBN;
+        mma_tf32_kloop(d, pl, vh, D, kBN, C::kIdescO, (j % C::kFlush) != 0);
+        mma_tf32_kloop(d, ph, vl, D, kBN, C::kIdescO, true);
+        mma_tf32_kloop(d, ph, vh, D, kBN, C::kIdescO, true);
+        ptx::mma_commit(&vempty[st]);
+        ptx::mma_commit(oready);
+        if (j == ntiles - 1) ptx::mma_commit(ofinal);
+      }
+      __syncwarp();
+    };
+    if (ntiles > 0) {
+      TF32_WAIT(qready, 0, 600);
+      ptx::tc_fence_after();
+      issue_qk(0);
+      if (ntiles > 1) issue_qk(1);
+      for (int j = 0; j < ntiles; ++j) {
+        issue_pv(j);
+        if (j + 2 < ntiles) issue_qk(j + 2);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- softmax + epilogue: thread <-> TMEM lane <-> query row
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;
+    const int64_t row = m0 + r;
+    const bool row_ok = row < Lq;
+    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t tl = tmem + lane_addr;
+    if (ntiles > 0) {
+      // Q row -> TMEM hi / lo (rows past Lq are zero)
+      const float4* qr = reinterpret_cast<const float4*>(q + (row * H + head) * D);
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
-        float o[32];
-        ptx::tmem_ld32(tO + c * 32, o);
-        ptx::tmem_wait_ld();
+        float hi[32], lo[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) o[e] *= alpha;
-        ptx::tmem_st32(tO + c * 32, o);
+        for (int e = 0; e < 8; ++e) {
+          const float4 x = row_ok ? qr[c * 8 + e] : make_float4(0.f, 0.f, 0.f, 0.f);
+          split_tf32(x.x, hi[4 * e], lo[4 * e]);
+          split_tf32(x.y, hi[4 * e + 1], lo[4 * e + 1]);
+          split_tf32(x.z, hi[4 * e + 2], lo[4 * e + 2]);
+          split_tf32(x.w, hi[4 * e + 3], lo[4 * e + 3]);
+        }
+        ptx::tmem_st32(tl + C::cQh + c * 32, hi);
+        ptx::tmem_st32(tl + C::cQl + c * 32, lo);
       }
       ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(qready);
     }
-    m_run = m_new;
-    ptx::fence_proxy_async_smem();
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (tid < 32) {
-      if (tid == 0) {
-        ptx::tc_fence_after();
-        const uint32_t d = tmem + C::kTmemO;
-        mma_tf32_kloop(d, sbase + C::kPl, kBM, sbase + C::kVh, D, kBN, C::kIdescO, jt > 0);
-        mma_tf32_kloop(d, sbase + C::kPh, kBM, sbase + C::kVl, D, kBN, C::kIdescO, true);
-        mma_tf32_kloop(d, sbase + C::kPh, kBM, sbase + C::kVh, D, kBN, C::kIdescO, true);
-        ptx::mma_commit(bar);
-      }
-      __syncwarp();
-    }
-    TF32_WAIT(bar, phase, 2000 + jt);  // PV done: K/V/P buffers free, O complete
-    phase ^= 1;
-    ptx::tc_fence_after();
-  }
-  // ---- epilogue: O / l, lse = ln l + m (natural log of the scaled scores)
-  const bool empty = !(l_run > 0.f);
-  const float inv = empty ? 0.f : 1.f / l_run;
+    // O = master + TMEM partial.  The tensor core's fp32 accumulation
+    // truncates, and its bias grows with the number of accumulate steps
+    // (measured: rel L2 1.1e-4 at 16384 keys with one accumulator); moving
+    // the partial into the master with round-to-nearest FADDs every kFlush
+    // tiles bounds that to kFlush tiles' worth.
+    float4* mrow = reinterpret_cast<float4*>(sm + C::kMOff + static_cast<size_t>(r) * D * 4);
 #pragma unroll
-  for (int c = 0; c < D / 32; ++c) {
-    float o[32];
-    if (ntiles > 0) {
-      ptx::tmem_ld32(tO + c * 32, o);
+    for (int c4 = 0; c4 < D / 4; ++c4) mrow[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t qp = pos_tf(qmap, row_ok ? row : Lq - 1);
+    const int64_t klim = klimit_tf(causal, kmap, Lk, qp);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int b = j & 1;
+      TF32_WAIT(&sfull[b], (j >> 1) & 1, 700);
+      ptx::tc_fence_after();
+      float s[kBN];
+#pragma unroll
+      for (int c = 0; c < kBN / 32; ++c)
+        ptx::tmem_ld32(tl + C::cS + b * kBN + c * 32, *reinterpret_cast<float(*)[32]>(&s[32 * c]));
       ptx::tmem_wait_ld();
-    } else {
+      const int64_t nv = klim - static_cast<int64_t>(j) * kBN;
+      float mx = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) o[e] = 0.f;
-    }
-    if (row_ok) {
-      float4* dst = reinterpret_cast<float4*>(out + (row * H + head) * D + c * 32);
+      for (int c = 0; c < kBN; ++c) {
+        s[c] = (c < nv) ? s[c] * scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[c]);
+      }
+      // lazy rescale: move the reference max only when a score exceeds it by
+      // more than 2^8 (P <= 256 otherwise); warp-uniform because the O
+      // rescale is a warp-collective tcgen05.ld / st
+      const bool need = mx > m_run + kTf32RescaleThreshold;
+      const bool rescale = __any_sync(0xffffffffu, need);
+      const bool flush = j > 0 && (j % C::kFlush) == 0;  // PV(j) restarts the accumulator
+      float alpha = 1.f;
+      if (rescale) {
+        const float m_new = fmaxf(m_run, mx);
+        alpha = (m_run == -INFINITY) ? 1.f : exp2f(m_run - m_new);
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      if (j > 0 && (rescale || flush)) {
+        // PV(j-1) complete: O is final so far.  Unambiguous parity: S(j)'s
+        // commit covered PV(j-2), and PV(j) waits for this tile's P.
+        TF32_WAIT(oready, (j - 1) & 1, 800);
+        ptx::tc_fence_after();
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv,
-                             o[4 * e + 3] * inv);
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          ptx::tmem_ld32(tl + C::cO + c * 32, o);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e4 = 0; e4 < 8; ++e4) {
+            float4& m = mrow[(c * 8 + e4) ^ (r & 7)];
+            if (flush) {  // master = (master + partial) * alpha
+              m = make_float4((m.x + o[4 * e4]) * alpha, (m.y + o[4 * e4 + 1]) * alpha,
+                              (m.z + o[4 * e4 + 2]) * alpha, (m.w + o[4 * e4 + 3]) * alpha);
+            } else {
+              m = make_float4(m.x * alpha, m.y * alpha, m.z * alpha, m.w * alpha);
+            }
+          }
+          if (!flush) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= alpha;
+            ptx::tmem_st32(tl + C::cO + c * 32, o);
+          }
+        }
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < kBN / 32; ++c) {
+        float hi[32], lo[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float p = exp2f(s[32 * c + e] - m_use);
+          sum += p;
+          split_tf32(p, hi[e], lo[e]);
+        }
+        ptx::tmem_st32(tl + C::cS + b * kBN + c * 32, hi);  // P hi over S(j)
+        ptx::tmem_st32(tl + C::cPl + b * kBN + c * 32, lo);
+      }
+      l_run += sum;
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&pready[b]);
     }
+    // ---- epilogue: O / l, lse = ln l + m (natural log of the scaled scores)
+    // (ofinal, not oready: up to two PVs may be outstanding here, so an
+    // oready parity would be ambiguous)
+    if (ntiles > 0) {
+      TF32_WAIT(ofinal, 0, 900);
+      ptx::tc_fence_after();
+    }
+    const bool empty = !(l_run > 0.f);
+    const float inv = empty ? 0.f : 1.f / l_run;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      float o[32];
+      if (ntiles > 0) {
+        ptx::tmem_ld32(tl + C::cO + c * 32, o);
+        ptx::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = 0.f;
+      }
+      if (row_ok) {
+        float4* dst = reinterpret_cast<float4*>(out + (row * H + head) * D + c * 32);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float4 m = mrow[(c * 8 + e) ^ (r & 7)];
+          dst[e] = make_float4((m.x + o[4 * e]) * inv, (m.y + o[4 * e + 1]) * inv,
+                               (m.z + o[4 * e + 2]) * inv, (m.w + o[4 * e + 3]) * inv);
+        }
+      }
+    }
+    if (row_ok)
+      lse[static_cast<int64_t>(head) * Lq + row] =
+          empty ? -INFINITY : (m_run + log2f(l_run)) * 0.69314718055994530942f;
   }
-  if (row_ok)
-    lse[static_cast<int64_t>(head) * Lq + row] =
-        empty ? -INFINITY : (m_run + log2f(l_run)) * 0.69314718055994530942f;
   ptx::tc_fence_before();
   __syncthreads();
-  if (tid < 32) {
+  if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<256>(tmem);
+    ptx::tmem_dealloc<512>(tmem);
   }
 }
+
+int64_t lk4_of(int64_t Lk) { return (Lk + 3) / 4 * 4; }
 
 template <int D>
 cudaError_t launch_tf32(const LocalAttnArgs& a, cudaStream_t stream) {
   using C = Tf32Cfg<D>;
+  if (a.Lk > 0 && (!a.scratch || a.scratch_bytes < tf32_scratch_bytes(a.Lk, a.H, D)))
+    return cudaErrorInvalidValue;
+  const int64_t Lk4 = lk4_of(a.Lk);
+  const size_t kel = static_cast<size_t>(a.Lk) * a.H * D, vel = static_cast<size_t>(a.H) * D * Lk4;
+  float* kh = static_cast<float*>(a.scratch);
+  float* kl = kh + kel;
+  float* vth = kl + kel;
+  float* vtl = vth + vel;
+  if (a.Lk > 0) {
+    dim3 g1(static_cast<unsigned>((a.Lk + 31) / 32), a.H);
+    tf32_split_kv_kernel<D><<<g1, 256, 0, stream>>>(static_cast<const float*>(a.k),
+                                                    static_cast<const float*>(a.v), kh, kl, vth,
+                                                    vtl, a.Lk, Lk4, a.H);
+  }
+  // K hi / lo: [Lk, H, D] as (D, H, Lk), boxes of 32 fp32 x 1 head x kBN keys;
+  // V^T hi / lo: [H, D, Lk4] as (Lk, D, H), boxes of 32 keys x D rows x 1 head
+  // (keys past Lk read as zeros).  128-byte swizzle, as the descriptors expect.
+  const cuuint64_t lk = static_cast<cuuint64_t>(a.Lk > 0 ? a.Lk : 1);
+  const cuuint64_t kdims[3] = {D, static_cast<cuuint64_t>(a.H), lk};
+  const cuuint64_t kstr[2] = {D * 4ull, static_cast<cuuint64_t>(a.H) * D * 4};
+  const cuuint32_t kbox[3] = {32, 1, static_cast<cuuint32_t>(C::kBN)};
+  const cuuint64_t vdims[3] = {lk, D, static_cast<cuuint64_t>(a.H)};
+  const cuuint64_t vstr[2] = {static_cast<cuuint64_t>(Lk4) * 4, static_cast<cuuint64_t>(Lk4) * D * 4};
+  const cuuint32_t vbox[3] = {32, D, 1};
+  CUtensorMap tkh{}, tkl{}, tvh{}, tvl{};  // Lk = 0: no tile is loaded, maps unused
+  if (a.Lk > 0 && (!make_tma_map_f32(&tkh, kh, kdims, kstr, kbox) ||
+                   !make_tma_map_f32(&tkl, kl, kdims, kstr, kbox) ||
+                   !make_tma_map_f32(&tvh, vth, vdims, vstr, vbox) ||
+                   !make_tma_map_f32(&tvl, vtl, vdims, vstr, vbox)))
+    return cudaErrorInvalidValue;
   static int attr_dev = -1;
   int cur = 0;
   cudaGetDevice(&cur);
@@ -312,14 +543,19 @@ cudaError_t launch_tf32(const LocalAttnArgs& a, cudaStream_t stream) {
     attr_dev = cur;
   }
   dim3 grid(static_cast<unsigned>((a.Lq + kBM - 1) / kBM), a.H);
-  attn_fwd_tf32x3_kernel<D><<<grid, 128, C::kSmem, stream>>>(
-      static_cast<const float*>(a.q), static_cast<const float*>(a.k),
-      static_cast<const float*>(a.v), static_cast<float*>(a.out), a.lse, a.Lq, a.Lk, a.H, a.causal,
-      a.qmap, a.kmap, static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))));
+  attn_fwd_tf32x3_kernel<D><<<grid, 256, C::kSmem, stream>>>(
+      tkh, tkl, tvh, tvl, static_cast<const float*>(a.q), static_cast<float*>(a.out), a.lse, a.Lq,
+      a.Lk, a.H, a.causal, a.qmap, a.kmap,
+      static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))));
   return cudaGetLastError();
 }
 
 }  // namespace
+
+size_t tf32_scratch_bytes(int64_t Lk, int H, int D) {
+  if (Lk <= 0) return 0;
+  return (2 * static_cast<size_t>(Lk) * H * D + 2 * static_cast<size_t>(H) * D * lk4_of(Lk)) * 4;
+}
 
 cudaError_t launch_attn_fwd_tf32x3(const LocalAttnArgs& a, cudaStream_t stream) {
   if (a.Lq <= 0) return cudaSuccess;

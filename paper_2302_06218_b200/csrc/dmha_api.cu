@@ -94,6 +94,9 @@ struct State {
   size_t mha_bytes = 0;
   void* sel = nullptr;  // NEXT-4 selector workspace
   size_t sel_bytes = 0;
+  // fp32 path: split K / V^T operands of the current key block (3xTF32)
+  void* tf32 = nullptr;
+  size_t tf32_bytes = 0;
   // host-path staging
   void* st_qkv = nullptr;  // q, k, v back to back
   void* st_out = nullptr;
@@ -190,7 +193,8 @@ void update_ws_stat() {
   g.stats.workspace_bytes = 2 * g.kv_bytes + (g.acc_elems + g.part_elems) * 4 +
                             (g.lse_elems + g.part_lse_elems) * 4 +
                             g.st_bytes + g.st_lse_elems * 4 + g.hp_bytes + g.mha_bytes +
-                            g.sel_bytes + (g.peer ? dmha::peer_pub_bytes(g.peer) : 0);
+                            g.sel_bytes + g.tf32_bytes +
+                            (g.peer ? dmha::peer_pub_bytes(g.peer) : 0);
 }
 
 int alloc_or_oom(void** p, size_t bytes, const char* what) {
@@ -230,11 +234,25 @@ bool split_kv_active(int64_t Lloc, int D, int H) {
 size_t ring_ws_bytes(int P, int64_t Lloc, int D, int H) {
   const size_t elems = static_cast<size_t>(Lloc) * H * D;
   const size_t lse = static_cast<size_t>(Lloc) * H;
-  if (P == 1) return split_kv_active(Lloc, D, H) ? 2 * (elems * 4 + lse * 4) : 0;
+  // fp32: the 3xTF32 split operands of one key block (at most Lloc keys)
+  const size_t tf32 = g.dtype == DMHA_FP32 ? dmha::tf32_scratch_bytes(Lloc, H, D) : 0;
+  if (P == 1) return (split_kv_active(Lloc, D, H) ? 2 * (elems * 4 + lse * 4) : 0) + tf32;
   const size_t parts = fused_combine(D) ? 1 : 2;
   // + the published K/V block of the peer transport (NEXT-2)
   const size_t pub = g.transport == 1 ? 2 * elems * elem_bytes(g.dtype) : 0;
-  return 2 * (2 * elems * elem_bytes(g.dtype)) + parts * (elems * 4 + lse * 4) + pub;
+  return 2 * (2 * elems * elem_bytes(g.dtype)) + parts * (elems * 4 + lse * 4) + pub + tf32;
+}
+
+// fp32 path scratch for a key block of Lk rows (grow-only).
+int ensure_tf32_ws(int64_t Lk, int D, int H) {
+  const size_t need = dmha::tf32_scratch_bytes(Lk, H, D);
+  if (need <= g.tf32_bytes) return DMHA_OK;
+  free_ptr(g.tf32);
+  g.tf32_bytes = 0;
+  int rc = alloc_or_oom(&g.tf32, need, "fp32 split K/V scratch");
+  if (rc == DMHA_OK) g.tf32_bytes = need;
+  update_ws_stat();
+  return rc;
 }
 
 // Ring accumulators (always), the partial buffers (unfused combine only) and
@@ -389,6 +407,11 @@ int run_local(const void* q, const void* k, const void* v, void* out, float* lse
   a.qmap = qm;
   a.kmap = km;
   a.out_mode = out_mode;
+  if (g.dtype == DMHA_FP32) {
+    if (int rc = ensure_tf32_ws(Lk, D, H)) return rc;
+    a.scratch = g.tf32;
+    a.scratch_bytes = g.tf32_bytes;
+  }
   cudaError_t e = cudaSuccess;
   timed(0, g.stream, [&]() {
     e = g.dtype == DMHA_BF16 ? dmha::launch_attn_fwd_bf16(a, g.stream)
@@ -397,7 +420,8 @@ int run_local(const void* q, const void* k, const void* v, void* out, float* lse
   });
   if (e != cudaSuccess)
     return fail(DMHA_ERR_CUDA, "dmha: attention kernel launch failed: %s", cudaGetErrorString(e));
-  g.stats.kernel_launches += dmha::attn_launches_per_call();
+  g.stats.kernel_launches += g.dtype == DMHA_BF16 ? dmha::attn_launches_per_call()
+                                                  : dmha::fp32_launches_per_call(Lq, Lk);
   return DMHA_OK;
 }
 
@@ -872,6 +896,7 @@ int dmha_finalize(void) {
   free_ptr(g.sel);
   free_ptr(g.hp);
   free_ptr(g.mha);
+  free_ptr(g.tf32);
   resolve_profiles();
   for (cudaEvent_t e : g.pool) cudaEventDestroy(e);
   g.pool.clear();
@@ -913,6 +938,8 @@ int dmha_reserve(int world_size, int64_t L, int D, int H) {
     return fail(DMHA_ERR_INVALID, "dmha_reserve: bad args");
   if (D != 64 && D != 128) return fail(DMHA_ERR_UNSUPPORTED, "dmha_reserve: D=%d", D);
   const int64_t Lloc = max_shard_rows(L, world_size, g.layout);
+  if (g.dtype == DMHA_FP32)
+    if (int rc = ensure_tf32_ws(Lloc, D, H)) return rc;
   if (world_size == 1) {
     if (split_kv_active(Lloc, D, H)) return ensure_ring_ws(Lloc, D, H, false, true);
     return DMHA_OK;
@@ -1263,7 +1290,6 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
   begin_forward();
   char* base = static_cast<char*>(g.hp);
   auto ws_of = [&](int r) { return base + static_cast<size_t>(r) * y.total; };
-  auto nothing = []() -> int { return DMHA_OK; };
   // Phase 1: every rank packs; the all-to-all is P*P device copies.
   for (int r = 0; r < P; ++r) {
     const dmha::HeadparGeom geo{P, H, D, Lloc, layout == DMHA_LAYOUT_ZIGZAG ? 1 : 0};
@@ -1298,7 +1324,6 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void* q, con
                                           static_cast<int>(e), g.stream),
             hp_out_bytes(Lloc, H, D, e, true));
   }
-  (void)nothing;
   // Phase 3: all-to-all back (out blocks and lse blocks), unpack per rank.
   for (int s = 0; s < P; ++s)
     for (int d = 0; d < P; ++d) {

@@ -42,6 +42,10 @@ struct LocalAttnArgs {
   // Fault injection only (DMHA_FAULT=perturb_lse, dmha.h): added to the
   // partial's lse inside the log-sum-exp combine; 0 in normal operation.
   float lse_bias = 0.f;
+  // fp32 path (3xTF32): caller-owned device scratch for the split K / V^T
+  // operands, at least tf32_scratch_bytes(Lk, H, D) bytes.
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
 };
 
 // bf16 tcgen05/TMEM/TMA flash-attention forward (attn_fwd_sm100.cu): two
@@ -56,6 +60,12 @@ bool attn_kv_split_supported(int D);
 // DMHA_FP32_SIMT=1 the SIMT fp32 kernel (attn_fwd_fp32.cu).
 cudaError_t launch_attn_fwd_fp32(const LocalAttnArgs& a, cudaStream_t stream);
 cudaError_t launch_attn_fwd_tf32x3(const LocalAttnArgs& a, cudaStream_t stream);
+// Scratch the 3xTF32 path needs for Lk keys: K hi / lo [Lk, H, D] and V^T
+// hi / lo [H, D, Lk rounded up to 4], fp32 (0 for Lk = 0).
+size_t tf32_scratch_bytes(int64_t Lk, int H, int D);
+// Kernel launches one fp32-path local attention call makes (the 3xTF32 path:
+// split + attention; the SIMT cross-check: one).
+int fp32_launches_per_call(int64_t Lq, int64_t Lk);
 // log-sum-exp combine (lse_combine.cu).  out_dtype_bf16 selects the final
 // output element type when final_step != 0.
 cudaError_t launch_lse_combine(float* o_acc, float* lse_acc, const float* o_part,

@@ -47,4 +47,17 @@ inline bool make_tma_map_bf16(CUtensorMap* map, const void* base, int64_t L, int
          CUDA_SUCCESS;
 }
 
+// Generic 3-D fp32 map (dims innermost first, byte strides of dims 1 and 2)
+// with the 128-byte swizzle; the 3xTF32 path's split K and V^T operands.
+inline bool make_tma_map_f32(CUtensorMap* map, const void* base, const cuuint64_t (&dims)[3],
+                             const cuuint64_t (&strides)[2], const cuuint32_t (&box)[3]) {
+  EncodeTiledFn enc = tma_encode_fn();
+  if (!enc) return false;
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 }  // namespace dmha

@@ -253,7 +253,9 @@ def test_workspace_bytes_equal_what_is_held(oracle_mod, case):
             e = 2 if dtype == "bf16" else 4
             Ll = L // P
             parts = 1 if dtype == "bf16" else 2  # fused combine only on the bf16 path
-            assert want == 4 * Ll * H * D * e + parts * (Ll * H * D * 4 + Ll * H * 4)
+            # fp32: + the 3xTF32 split K hi/lo [Ll, H, D] and V^T hi/lo [H, D, Ll up to x4]
+            tf32 = 0 if dtype == "bf16" else 2 * Ll * H * D * 4 + 2 * H * D * (-(-Ll // 4) * 4) * 4
+            assert want == 4 * Ll * H * D * e + parts * (Ll * H * D * 4 + Ll * H * 4) + tf32
         assert dmha.get_stats()["workspace_bytes"] == want
     finally:
         dmha.finalize()
@@ -498,7 +500,7 @@ def test_d128_schedules_on_the_ring(lib_bf16, oracle_mod, monkeypatch, env, P, l
 
 
 FP32_SHAPES = [(1, 1, 64), (37, 2, 64), (128, 1, 128), (200, 3, 128), (512, 4, 64), (777, 2, 64),
-               (1000, 2, 128)]
+               (1000, 2, 128), (4133, 2, 64), (2085, 2, 128)]
 
 
 @pytest.mark.parametrize("simt", [False, True])
@@ -515,6 +517,26 @@ def test_fp32_path_tf32x3_and_simt(oracle_mod, monkeypatch, simt, causal, L, H, 
     out, lse = run_p1(q, k, v, causal, torch.float32)
     ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
     assert_parity(out, lse, ref_o, ref_l, "fp32", f"fp32 simt={simt} L={L} H={H} D={D} causal={causal}")
+
+
+@pytest.mark.parametrize("L,H,D,causal", [(16384, 8, 64, False), (16384, 8, 64, True),
+                                          (8269, 4, 128, True)])
+def test_fp32_path_large_sampled(oracle_mod, L, H, D, causal):
+    """The fp32 path at C2's shape in fp32 (and D = 128 with a ragged tail):
+    hundreds of key tiles through the 3xTF32 kernel's K / V^T rings, the
+    double-buffered S / P and the lazy rescale; sampled rows (first / last
+    128, CTA boundaries, random) against the fp64 oracle over all keys at the
+    fp32 tolerance."""
+    ensure_lib("fp32")
+    q, k, v = inputs.qkv(L, H, D, seed=3100 + D + int(causal), dtype="fp32")
+    out, lse = run_p1(q, k, v, causal, torch.float32)
+    rows = set(range(128)) | set(range(L - 128, L))
+    for b in range(128, L, 128 * 13):
+        rows |= {b - 1, b}
+    rows |= set(np.random.default_rng(7).integers(0, L, 64).tolist())
+    rows = np.array(sorted(rows), dtype=np.int64)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal, rows=rows)
+    assert_parity(out[rows], lse[:, rows], ref_o, ref_l, "fp32", f"fp32 L={L} H={H} D={D} causal={causal}")
 
 
 def test_fp32_tf32x3_beats_one_pass_tf32_bound(oracle_mod):
