@@ -125,26 +125,44 @@ __device__ __forceinline__ int64_t klimit_tf(int causal, const PosMap& km, int64
   return lim < Lk ? lim : Lk;
 }
 
-// D[tmem] (+)= A[tmem] * B[smem desc]  (kind::tf32, A read from tensor memory)
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
+// D[tmem] (+)= A[tmem] * B[smem desc]  (kind::tf32, A read from tensor
+// memory).  Whole-warp issue: every lane of the converged issuer warp runs it
+// with the same operands and elect.sync picks the issuing lane; the smem
+// descriptor is given as its low word (start address >> 4 | LBO) plus the
+// constant high word, so per-MMA descriptor math is one 32-bit add.  The
+// issue rate matters here: a 128 x 64 x 8 tf32 MMA is ~32 tensor cycles (16
+// at N = 32), and a one-thread loop building 64-bit descriptors per MMA
+// measured slower than that (tensor pipe 36 % active, softmax starved).
+__device__ __forceinline__ void mma_tf32_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo,
+                                              uint32_t desc_hi, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 db;\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], db, %4, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "r"(b_lo), "r"(desc_hi), "r"(idesc), "r"(acc)
       : "memory");
 }
 
-// D (+)= A * B^T over K = kdim: A = kdim TMEM columns from a_col, B = a
-// K-major 128-byte-swizzled shared-memory operand of b_rows rows (panels of
-// 32 fp32 along K).  Eight K elements per instruction.
-__device__ __forceinline__ void mma_tf32_kloop(uint32_t d, uint32_t a_col, uint32_t b, int b_rows,
-                                               int kdim, uint32_t idesc, bool acc) {
-  for (int kk = 0; kk < kdim / 8; ++kk) {
-    const uint32_t off = (kk >> 2) * b_rows * 128 + (kk & 3) * 32;
-    mma_tf32_ts(d, a_col + kk * 8, ptx::smem_desc_sw128(b + off, 16, 1024), idesc,
-                (acc || kk > 0) ? 1u : 0u);
+// 128-byte-swizzle K-major smem descriptor words (SBO = 1024 B: 8 rows x 128 B)
+constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+__device__ __forceinline__ uint32_t desc_lo(uint32_t saddr) {
+  return ((saddr >> 4) & 0x3FFFu) | (1u << 16);  // LBO = 16 B (unused with swizzle)
+}
+
+// D (+)= A * B^T over K = kKdim: A = kKdim TMEM columns from a_col, B = a
+// K-major 128-byte-swizzled shared-memory operand of kBRows rows (panels of
+// 32 fp32 along K) whose descriptor low word is b_lo.  Eight K elements per
+// instruction, fully unrolled (constant descriptor offsets).
+template <int kKdim, int kBRows>
+__device__ __forceinline__ void mma_tf32_kloop(uint32_t d, uint32_t a_col, uint32_t b_lo,
+                                               uint32_t idesc, bool acc) {
+#pragma unroll
+  for (int kk = 0; kk < kKdim / 8; ++kk) {
+    constexpr int kPanel = kBRows * 128;
+    const uint32_t off = static_cast<uint32_t>((kk >> 2) * kPanel + (kk & 3) * 32) >> 4;
+    mma_tf32_ts_w(d, a_col + kk * 8, b_lo + off, kDescHi, idesc, (acc || kk > 0) ? 1u : 0u);
   }
 }
 
@@ -297,21 +315,21 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: QK(0), QK(1), then PV(j), QK(j+2) ...  One lane
-    // issues; the warp waits on the barriers together (no lane spins alone).
+    // ---- MMA issuer: QK(0), QK(1), then PV(j), QK(j+2) ...  The whole warp
+    // waits on the barriers and runs the issue code; elect.sync picks the
+    // lane that issues (no lane spins alone, descriptors stay uniform).
     auto issue_qk = [&](int j) {
       const int st = j % kKST;
       TF32_WAIT(&kfull[st], (j / kKST) & 1, 300);
       ptx::tc_fence_after();
-      if (lane == 0) {
-        const uint32_t d = tmem + C::cS + (j & 1) * kBN;
-        const uint32_t kh = sbase + C::kKOff + st * 2 * C::kKOp, kl = kh + C::kKOp;
-        mma_tf32_kloop(d, tmem + C::cQl, kh, kBN, D, C::kIdescS, false);
-        mma_tf32_kloop(d, tmem + C::cQh, kl, kBN, D, C::kIdescS, true);
-        mma_tf32_kloop(d, tmem + C::cQh, kh, kBN, D, C::kIdescS, true);
-        ptx::mma_commit(&kempty[st]);
-        ptx::mma_commit(&sfull[j & 1]);
-      }
+      const uint32_t d = tmem + C::cS + (j & 1) * kBN;
+      const uint32_t kh = desc_lo(sbase + C::kKOff + st * 2 * C::kKOp);
+      const uint32_t kl = kh + (C::kKOp >> 4);
+      mma_tf32_kloop<D, kBN>(d, tmem + C::cQl, kh, C::kIdescS, false);
+      mma_tf32_kloop<D, kBN>(d, tmem + C::cQh, kl, C::kIdescS, true);
+      mma_tf32_kloop<D, kBN>(d, tmem + C::cQh, kh, C::kIdescS, true);
+      ptx::mma_commit_w(&kempty[st]);
+      ptx::mma_commit_w(&sfull[j & 1]);
       __syncwarp();
     };
     auto issue_pv = [&](int j) {
@@ -319,17 +337,16 @@ __global__ void __launch_bounds__(256, 1)
       TF32_WAIT(&pready[b], (j >> 1) & 1, 400);
       TF32_WAIT(&vfull[st], (j / kVST) & 1, 500);
       ptx::tc_fence_after();
-      if (lane == 0) {
-        const uint32_t d = tmem + C::cO;
-        const uint32_t vh = sbase + C::kVOff + st * 2 * C::kVOp, vl = vh + C::kVOp;
-        const uint32_t ph = tmem + C::cS + b * kBN, pl = tmem + C::cPl + b * kBN;
-        mma_tf32_kloop(d, pl, vh, D, kBN, C::kIdescO, (j % C::kFlush) != 0);
-        mma_tf32_kloop(d, ph, vl, D, kBN, C::kIdescO, true);
-        mma_tf32_kloop(d, ph, vh, D, kBN, C::kIdescO, true);
-        ptx::mma_commit(&vempty[st]);
-        ptx::mma_commit(oready);
-        if (j == ntiles - 1) ptx::mma_commit(ofinal);
-      }
+      const uint32_t d = tmem + C::cO;
+      const uint32_t vh = desc_lo(sbase + C::kVOff + st * 2 * C::kVOp);
+      const uint32_t vl = vh + (C::kVOp >> 4);
+      const uint32_t ph = tmem + C::cS + b * kBN, pl = tmem + C::cPl + b * kBN;
+      mma_tf32_kloop<kBN, D>(d, pl, vh, C::kIdescO, (j % C::kFlush) != 0);
+      mma_tf32_kloop<kBN, D>(d, ph, vl, C::kIdescO, true);
+      mma_tf32_kloop<kBN, D>(d, ph, vh, C::kIdescO, true);
+      ptx::mma_commit_w(&vempty[st]);
+      ptx::mma_commit_w(oready);
+      if (j == ntiles - 1) ptx::mma_commit_w(ofinal);
       __syncwarp();
     };
     if (ntiles > 0) {
