@@ -106,6 +106,19 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ int64_t pos_tf(const PosMap& m, int64_t i) {
   return i < m.chunk ? m.base0 + i : m.base1 + (i - m.chunk);
 }
@@ -393,9 +406,11 @@ __global__ void __launch_bounds__(256, 1)
     // (measured: rel L2 1.1e-4 at 16384 keys with one accumulator); moving
     // the partial into the master with round-to-nearest FADDs every kFlush
     // tiles bounds that to kFlush tiles' worth.
-    float4* mrow = reinterpret_cast<float4*>(sm + C::kMOff + static_cast<size_t>(r) * D * 4);
+    // (16-byte chunk c4 of this row's master at mrow + 16 * (c4 ^ (r & 7)))
+    const uint32_t mrow = sbase + C::kMOff + static_cast<uint32_t>(r) * D * 4;
+    auto mchunk = [&](int c4) { return mrow + static_cast<uint32_t>((c4 ^ (r & 7)) << 4); };
 #pragma unroll
-    for (int c4 = 0; c4 < D / 4; ++c4) mrow[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c4 = 0; c4 < D / 4; ++c4) sts128(mrow + c4 * 16, make_float4(0.f, 0.f, 0.f, 0.f));
     const int64_t qp = pos_tf(qmap, row_ok ? row : Lq - 1);
     const int64_t klim = klimit_tf(causal, kmap, Lk, qp);
     float m_run = -INFINITY, l_run = 0.f;
@@ -408,13 +423,22 @@ __global__ void __launch_bounds__(256, 1)
       for (int c = 0; c < kBN / 32; ++c)
         ptx::tmem_ld32(tl + C::cS + b * kBN + c * 32, *reinterpret_cast<float(*)[32]>(&s[32 * c]));
       ptx::tmem_wait_ld();
+      // row max of the raw scores (the scale is positive), 8 independent
+      // partial maxima (one softmax warp per SMSP: latency, not issue, binds);
+      // keys past the row's limit (causal / ragged tail) are -inf
       const int64_t nv = klim - static_cast<int64_t>(j) * kBN;
-      float mx = -INFINITY;
+      if (nv < kBN) {
 #pragma unroll
-      for (int c = 0; c < kBN; ++c) {
-        s[c] = (c < nv) ? s[c] * scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s[c]);
+        for (int c = 0; c < kBN; ++c) s[c] = (c < nv) ? s[c] : -INFINITY;
       }
+      float pm[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pm[i] = s[i];
+#pragma unroll
+      for (int c = 8; c < kBN; ++c) pm[c & 7] = fmaxf(pm[c & 7], s[c]);
+      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) *
+                       scale_log2;
       // lazy rescale: move the reference max only when a score exceeds it by
       // more than 2^8 (P <= 256 otherwise); warp-uniform because the O
       // rescale is a warp-collective tcgen05.ld / st
@@ -440,12 +464,13 @@ __global__ void __launch_bounds__(256, 1)
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int e4 = 0; e4 < 8; ++e4) {
-            float4& m = mrow[(c * 8 + e4) ^ (r & 7)];
+            const uint32_t a = mchunk(c * 8 + e4);
+            const float4 m = lds128(a);
             if (flush) {  // master = (master + partial) * alpha
-              m = make_float4((m.x + o[4 * e4]) * alpha, (m.y + o[4 * e4 + 1]) * alpha,
-                              (m.z + o[4 * e4 + 2]) * alpha, (m.w + o[4 * e4 + 3]) * alpha);
+              sts128(a, make_float4((m.x + o[4 * e4]) * alpha, (m.y + o[4 * e4 + 1]) * alpha,
+                                    (m.z + o[4 * e4 + 2]) * alpha, (m.w + o[4 * e4 + 3]) * alpha));
             } else {
-              m = make_float4(m.x * alpha, m.y * alpha, m.z * alpha, m.w * alpha);
+              sts128(a, make_float4(m.x * alpha, m.y * alpha, m.z * alpha, m.w * alpha));
             }
           }
           if (!flush) {
@@ -455,21 +480,21 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float sum = 0.f;
+      const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
 #pragma unroll
       for (int c = 0; c < kBN / 32; ++c) {
         float hi[32], lo[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const float p = exp2f(s[32 * c + e] - m_use);
-          sum += p;
+          const float p = exp2f(fmaf(s[32 * c + e], scale_log2, neg_m));
+          ps[e & 3] += p;
           split_tf32(p, hi[e], lo[e]);
         }
         ptx::tmem_st32(tl + C::cS + b * kBN + c * 32, hi);  // P hi over S(j)
         ptx::tmem_st32(tl + C::cPl + b * kBN + c * 32, lo);
       }
-      l_run += sum;
+      l_run += (ps[0] + ps[1]) + (ps[2] + ps[3]);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&pready[b]);
@@ -497,7 +522,7 @@ __global__ void __launch_bounds__(256, 1)
         float4* dst = reinterpret_cast<float4*>(out + (row * H + head) * D + c * 32);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float4 m = mrow[(c * 8 + e) ^ (r & 7)];
+          const float4 m = lds128(mchunk(c * 8 + e));
           dst[e] = make_float4((m.x + o[4 * e]) * inv, (m.y + o[4 * e + 1]) * inv,
                                (m.z + o[4 * e + 2]) * inv, (m.w + o[4 * e + 3]) * inv);
         }
