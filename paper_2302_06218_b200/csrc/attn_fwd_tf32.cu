@@ -16,11 +16,13 @@
 //     reads both operands K-major, so V is transposed once here instead of in
 //     every CTA).
 //  2. attn_fwd_tf32x3_kernel: CTA = one 128-row query tile of one head,
-//     8 warps:
+//     12 warps (D = 64) / 8 warps (D = 128):
 //       warp 0     TMA producer of K hi / lo     (kKST-slot ring)
 //       warp 1     TMEM allocator + MMA issuer
 //       warp 2     TMA producer of V^T hi / lo   (kVST-slot ring)
-//       warps 4-7  softmax + epilogue (thread <-> TMEM lane <-> query row)
+//       warps 4-7  softmax + epilogue (thread <-> TMEM lane <-> query row);
+//                  D = 64: warps 4-7 and 8-11 each take half of every
+//                  row's score and output columns
 //     Both A operands live in TMEM (Q hi / lo written once by the softmax
 //     threads; P hi over the S columns it came from, P lo in its own
 //     columns), so the tensor core reads only the K / V^T tiles from shared
@@ -82,7 +84,14 @@ struct Tf32Cfg {
   // fp32 master copy of O (one 128-row tile; 16-byte chunks XOR-swizzled by
   // row so a warp's row-per-thread accesses are conflict-free)
   static constexpr int kMOff = kVOff + kVST * 2 * kVOp;
-  static constexpr int kBarOff = kMOff + kBM * D * 4;
+  // D = 64: two softmax warpgroups split each row's score columns (the
+  // per-row chain, not issue, bounds one warp per SMSP); they exchange row
+  // maxima (2 tiles x 2 halves x 128) and, at the end, row sums (2 x 128)
+  static constexpr int kHalves = D == 64 ? 2 : 1;
+  static constexpr int kThreads = 128 + 128 * kHalves;
+  static constexpr int kCols = kBN / kHalves;  // score columns per half
+  static constexpr int kRedOff = kMOff + kBM * D * 4;
+  static constexpr int kBarOff = kRedOff + (kHalves == 2 ? 6 * kBM * 4 : 0);
   // PV restarts its TMEM accumulator every kFlush tiles after the softmax
   // threads have added the partial into the master copy (see the kernel)
   static constexpr int kFlush = DMHA_TF32_FLUSH;
@@ -117,6 +126,15 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
                : "memory");
+}
+
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
 
 __device__ __forceinline__ int64_t pos_tf(const PosMap& m, int64_t i) {
@@ -227,7 +245,7 @@ __global__ void __launch_bounds__(256) tf32_split_kv_kernel(
 
 // ---------------------------------------------------------------- launch 2
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(Tf32Cfg<D>::kThreads, 1)
     attn_fwd_tf32x3_kernel(const __grid_constant__ CUtensorMap tm_kh,
                            const __grid_constant__ CUtensorMap tm_kl,
                            const __grid_constant__ CUtensorMap tm_vh,
@@ -271,11 +289,11 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&sfull[i], 1);
-      ptx::mbar_init(&pready[i], 128);
+      ptx::mbar_init(&pready[i], 128 * C::kHalves);
     }
     ptx::mbar_init(oready, 1);
     ptx::mbar_init(ofinal, 1);
-    ptx::mbar_init(qready, 128);
+    ptx::mbar_init(qready, 128 * C::kHalves);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
@@ -373,18 +391,24 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---- softmax + epilogue: thread <-> TMEM lane <-> query row
+    // ---- softmax + epilogue: thread <-> TMEM lane <-> query row.  With two
+    // halves (D = 64) warpgroup h owns score columns [32h, 32h + 32) of each
+    // tile and O / Q columns [32h, 32h + 32); the halves agree on the row max
+    // through shared memory once per tile (named barrier 1).
+    constexpr int kH = C::kHalves, kCols = C::kCols, kOCols = D / kH;
+    const int h = kH == 2 ? (warp - 4) >> 2 : 0;
     const int wq = warp & 3;
     const int r = wq * 32 + lane;
     const int64_t row = m0 + r;
     const bool row_ok = row < Lq;
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t tl = tmem + lane_addr;
+    const int scol = h * kCols, ocol = h * kOCols;
     if (ntiles > 0) {
       // Q row -> TMEM hi / lo (rows past Lq are zero)
-      const float4* qr = reinterpret_cast<const float4*>(q + (row * H + head) * D);
+      const float4* qr = reinterpret_cast<const float4*>(q + (row * H + head) * D + ocol);
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < kOCols / 32; ++c) {
         float hi[32], lo[32];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -394,8 +418,8 @@ __global__ void __launch_bounds__(256, 1)
           split_tf32(x.z, hi[4 * e + 2], lo[4 * e + 2]);
           split_tf32(x.w, hi[4 * e + 3], lo[4 * e + 3]);
         }
-        ptx::tmem_st32(tl + C::cQh + c * 32, hi);
-        ptx::tmem_st32(tl + C::cQl + c * 32, lo);
+        ptx::tmem_st32(tl + C::cQh + ocol + c * 32, hi);
+        ptx::tmem_st32(tl + C::cQl + ocol + c * 32, lo);
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
@@ -406,11 +430,13 @@ __global__ void __launch_bounds__(256, 1)
     // (measured: rel L2 1.1e-4 at 16384 keys with one accumulator); moving
     // the partial into the master with round-to-nearest FADDs every kFlush
     // tiles bounds that to kFlush tiles' worth.
-    // (16-byte chunk c4 of this row's master at mrow + 16 * (c4 ^ (r & 7)))
+    // (16-byte chunk c4 of this row's master at mrow + 16 * (c4 ^ (r & 7));
+    // the XOR keeps each half's chunks in its own half of the row)
     const uint32_t mrow = sbase + C::kMOff + static_cast<uint32_t>(r) * D * 4;
     auto mchunk = [&](int c4) { return mrow + static_cast<uint32_t>((c4 ^ (r & 7)) << 4); };
 #pragma unroll
-    for (int c4 = 0; c4 < D / 4; ++c4) sts128(mrow + c4 * 16, make_float4(0.f, 0.f, 0.f, 0.f));
+    for (int c4 = 0; c4 < kOCols / 4; ++c4) sts128(mchunk(ocol / 4 + c4), make_float4(0.f, 0.f, 0.f, 0.f));
+    const uint32_t red = sbase + C::kRedOff;  // [2 tiles][2 halves][kBM] maxima, then [2][kBM] sums
     const int64_t qp = pos_tf(qmap, row_ok ? row : Lq - 1);
     const int64_t klim = klimit_tf(causal, kmap, Lk, qp);
     float m_run = -INFINITY, l_run = 0.f;
@@ -418,30 +444,38 @@ __global__ void __launch_bounds__(256, 1)
       const int b = j & 1;
       TF32_WAIT(&sfull[b], (j >> 1) & 1, 700);
       ptx::tc_fence_after();
-      float s[kBN];
+      float s[kCols];
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c)
-        ptx::tmem_ld32(tl + C::cS + b * kBN + c * 32, *reinterpret_cast<float(*)[32]>(&s[32 * c]));
+      for (int c = 0; c < kCols / 32; ++c)
+        ptx::tmem_ld32(tl + C::cS + b * kBN + scol + c * 32,
+                       *reinterpret_cast<float(*)[32]>(&s[32 * c]));
       ptx::tmem_wait_ld();
       // row max of the raw scores (the scale is positive), 8 independent
-      // partial maxima (one softmax warp per SMSP: latency, not issue, binds);
+      // partial maxima (one softmax warp per SMSP per half: latency binds);
       // keys past the row's limit (causal / ragged tail) are -inf
-      const int64_t nv = klim - static_cast<int64_t>(j) * kBN;
-      if (nv < kBN) {
+      const int64_t nv = klim - static_cast<int64_t>(j) * kBN - scol;
+      if (nv < kCols) {
 #pragma unroll
-        for (int c = 0; c < kBN; ++c) s[c] = (c < nv) ? s[c] : -INFINITY;
+        for (int c = 0; c < kCols; ++c) s[c] = (c < nv) ? s[c] : -INFINITY;
       }
       float pm[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) pm[i] = s[i];
 #pragma unroll
-      for (int c = 8; c < kBN; ++c) pm[c & 7] = fmaxf(pm[c & 7], s[c]);
-      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) *
-                       scale_log2;
+      for (int c = 8; c < kCols; ++c) pm[c & 7] = fmaxf(pm[c & 7], s[c]);
+      float rmax = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                         fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      if constexpr (kH == 2) {
+        const uint32_t slot = red + static_cast<uint32_t>(((b * 2 + h) * kBM + r) * 4);
+        sts32(slot, rmax);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        rmax = fmaxf(rmax, lds32(red + static_cast<uint32_t>(((b * 2 + (h ^ 1)) * kBM + r) * 4)));
+      }
+      const float mx = rmax * scale_log2;
       // lazy rescale: move the reference max only when a score exceeds it by
       // more than 2^8 (P <= 256 otherwise); warp-uniform because the O
-      // rescale is a warp-collective tcgen05.ld / st
+      // rescale is a warp-collective tcgen05.ld / st, and the same in both
+      // halves (same rows, same max)
       const bool need = mx > m_run + kTf32RescaleThreshold;
       const bool rescale = __any_sync(0xffffffffu, need);
       const bool flush = j > 0 && (j % C::kFlush) == 0;  // PV(j) restarts the accumulator
@@ -458,13 +492,13 @@ __global__ void __launch_bounds__(256, 1)
         TF32_WAIT(oready, (j - 1) & 1, 800);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < kOCols / 32; ++c) {
           float o[32];
-          ptx::tmem_ld32(tl + C::cO + c * 32, o);
+          ptx::tmem_ld32(tl + C::cO + ocol + c * 32, o);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int e4 = 0; e4 < 8; ++e4) {
-            const uint32_t a = mchunk(c * 8 + e4);
+            const uint32_t a = mchunk(ocol / 4 + c * 8 + e4);
             const float4 m = lds128(a);
             if (flush) {  // master = (master + partial) * alpha
               sts128(a, make_float4((m.x + o[4 * e4]) * alpha, (m.y + o[4 * e4 + 1]) * alpha,
@@ -476,14 +510,14 @@ __global__ void __launch_bounds__(256, 1)
           if (!flush) {
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] *= alpha;
-            ptx::tmem_st32(tl + C::cO + c * 32, o);
+            ptx::tmem_st32(tl + C::cO + ocol + c * 32, o);
           }
         }
       }
       const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
       float ps[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) {
+      for (int c = 0; c < kCols / 32; ++c) {
         float hi[32], lo[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
@@ -491,8 +525,8 @@ __global__ void __launch_bounds__(256, 1)
           ps[e & 3] += p;
           split_tf32(p, hi[e], lo[e]);
         }
-        ptx::tmem_st32(tl + C::cS + b * kBN + c * 32, hi);  // P hi over S(j)
-        ptx::tmem_st32(tl + C::cPl + b * kBN + c * 32, lo);
+        ptx::tmem_st32(tl + C::cS + b * kBN + scol + c * 32, hi);  // P hi over S(j)
+        ptx::tmem_st32(tl + C::cPl + b * kBN + scol + c * 32, lo);
       }
       l_run += (ps[0] + ps[1]) + (ps[2] + ps[3]);
       ptx::tmem_wait_st();
@@ -506,31 +540,38 @@ __global__ void __launch_bounds__(256, 1)
       TF32_WAIT(ofinal, 0, 900);
       ptx::tc_fence_after();
     }
-    const bool empty = !(l_run > 0.f);
-    const float inv = empty ? 0.f : 1.f / l_run;
+    float l_tot = l_run;
+    if constexpr (kH == 2) {
+      const uint32_t lred = red + static_cast<uint32_t>(4 * kBM * 4);
+      sts32(lred + static_cast<uint32_t>((h * kBM + r) * 4), l_run);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      l_tot += lds32(lred + static_cast<uint32_t>(((h ^ 1) * kBM + r) * 4));
+    }
+    const bool empty = !(l_tot > 0.f);
+    const float inv = empty ? 0.f : 1.f / l_tot;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < kOCols / 32; ++c) {
       float o[32];
       if (ntiles > 0) {
-        ptx::tmem_ld32(tl + C::cO + c * 32, o);
+        ptx::tmem_ld32(tl + C::cO + ocol + c * 32, o);
         ptx::tmem_wait_ld();
       } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = 0.f;
       }
       if (row_ok) {
-        float4* dst = reinterpret_cast<float4*>(out + (row * H + head) * D + c * 32);
+        float4* dst = reinterpret_cast<float4*>(out + (row * H + head) * D + ocol + c * 32);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float4 m = lds128(mchunk(c * 8 + e));
+          const float4 m = lds128(mchunk(ocol / 4 + c * 8 + e));
           dst[e] = make_float4((m.x + o[4 * e]) * inv, (m.y + o[4 * e + 1]) * inv,
                                (m.z + o[4 * e + 2]) * inv, (m.w + o[4 * e + 3]) * inv);
         }
       }
     }
-    if (row_ok)
+    if (row_ok && h == 0)
       lse[static_cast<int64_t>(head) * Lq + row] =
-          empty ? -INFINITY : (m_run + log2f(l_run)) * 0.69314718055994530942f;
+          empty ? -INFINITY : (m_run + log2f(l_tot)) * 0.69314718055994530942f;
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -585,7 +626,7 @@ cudaError_t launch_tf32(const LocalAttnArgs& a, cudaStream_t stream) {
     attr_dev = cur;
   }
   dim3 grid(static_cast<unsigned>((a.Lq + kBM - 1) / kBM), a.H);
-  attn_fwd_tf32x3_kernel<D><<<grid, 256, C::kSmem, stream>>>(
+  attn_fwd_tf32x3_kernel<D><<<grid, C::kThreads, C::kSmem, stream>>>(
       tkh, tkl, tvh, tvl, static_cast<const float*>(a.q), static_cast<float*>(a.out), a.lse, a.Lq,
       a.Lk, a.H, a.causal, a.qmap, a.kmap,
       static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D))));
