@@ -136,24 +136,31 @@ def _check_tensors(tensors: dict, shapes: dict, dtypes: dict, device=None, pinne
     """Argument checks the kernels rely on (they assume contiguous rows of
     H*D elements and write exactly the documented sizes): every tensor is
     contiguous, has the expected shape and dtype, and lives on one CUDA
-    device (or in host memory for the host path)."""
+    device (or in host memory for the host path).  Messages are formatted
+    only on failure (this runs on every call; small forwards are host-bound)."""
     dev = None
     for name, t in tensors.items():
         if t is None:
             continue
-        _need(t.is_contiguous(), f"{name} must be contiguous (got strides {tuple(t.stride())})")
-        if name in shapes:
-            _need(tuple(t.shape) == tuple(shapes[name]),
-                  f"{name} has shape {tuple(t.shape)}, expected {tuple(shapes[name])}")
-        if name in dtypes:
-            _need(t.dtype == dtypes[name], f"{name} has dtype {t.dtype}, expected {dtypes[name]}")
+        if not t.is_contiguous():
+            raise DmhaError(ERR_INVALID, f"{name} must be contiguous (got strides {tuple(t.stride())})")
+        want = shapes.get(name)
+        if want is not None and t.shape != want:
+            raise DmhaError(ERR_INVALID, f"{name} has shape {tuple(t.shape)}, expected {tuple(want)}")
+        want = dtypes.get(name)
+        if want is not None and t.dtype != want:
+            raise DmhaError(ERR_INVALID, f"{name} has dtype {t.dtype}, expected {want}")
         if pinned:
-            _need(t.device.type == "cpu", f"{name} must be a host tensor for the host path")
+            if t.is_cuda:
+                raise DmhaError(ERR_INVALID, f"{name} must be a host tensor for the host path")
         else:
-            _need(t.is_cuda, f"{name} must be a CUDA tensor")
+            if not t.is_cuda:
+                raise DmhaError(ERR_INVALID, f"{name} must be a CUDA tensor")
+            d = t.get_device()
             if dev is None:
-                dev = t.device
-            _need(t.device == dev, f"{name} is on {t.device}, other arguments on {dev}")
+                dev = d
+            elif d != dev:
+                raise DmhaError(ERR_INVALID, f"{name} is on cuda:{d}, other arguments on cuda:{dev}")
 
 
 def _elem_dtype():
@@ -165,6 +172,9 @@ def _elem_dtype():
 
 def _cur_stream() -> int:
     import torch
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:  # no Stream object per call
+        return int(raw(torch.cuda.current_device()))
     return int(torch.cuda.current_stream().cuda_stream)
 
 
@@ -196,6 +206,7 @@ def init(world_size: int = 1, rank: int = 0, unique_id: bytes | None = None, dev
                            dtype_code(dtype), layout_code(layout), s))
     _STATE["dtype"] = dtype_code(dtype)
     _STATE["world"] = int(world_size)
+    _STATE["stream"] = s  # the stream dmha_init was given
 
 
 def init_distributed(dtype="bf16", layout="contiguous", device: int | None = None):
@@ -213,12 +224,18 @@ def init_distributed(dtype="bf16", layout="contiguous", device: int | None = Non
 
 
 def set_stream(stream: int):
-    _check(lib().dmha_set_stream(int(stream)))
+    """The stream every later call launches on (cached: the C call is made
+    only when it changes)."""
+    stream = int(stream)
+    if _STATE.get("stream") != stream:
+        _check(lib().dmha_set_stream(stream))
+        _STATE["stream"] = stream
 
 
 def finalize():
     _check(lib().dmha_finalize())
     _STATE["dtype"] = None
+    _STATE["stream"] = None
 
 
 def synchronize():

@@ -1,0 +1,2 @@
+#!/bin/bash
+python tools/host_overhead.py fp32; python tools/host_overhead.py bf16
