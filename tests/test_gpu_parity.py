@@ -623,3 +623,23 @@ def test_emulated_ring_uneven_shards(lib_bf16, oracle_mod, P, extra, causal, D):
     # sized by its owner
     sent = sum(rows[(r - s) % P] for r in range(P) for s in range(P - 1)) * H * D * 2 * 2
     assert dmha.get_stats()["last_bytes_sent"] == sent
+
+
+@pytest.mark.parametrize("P,layout,causal,D,extra", [(4, "zigzag", True, 64, 0),
+                                                     (3, "contiguous", True, 128, 2),
+                                                     (2, "contiguous", False, 64, 1)])
+def test_fp32_ring_emulated_many_tiles(oracle_mod, P, layout, causal, D, extra):
+    """The fp32 path (3xTF32 kernel + separate log-sum-exp combine) through the
+    emulated ring at sizes with many key tiles per step: zigzag key blocks
+    (two chunks per block, global-position causal limits inside a tile),
+    uneven contiguous shards, every step's split-operand pre-pass — against
+    the fp64 oracle at the fp32 tolerance."""
+    ensure_lib("fp32")
+    L, H = 1024 * P + extra, 2
+    q, k, v = inputs.qkv(L, H, D, seed=2700 + P + D, dtype="fp32")
+    parts = [dmha.stack_shards(x, P, layout) for x in (q, k, v)]
+    out, lse = dmha.forward_emulated(P, layout, *(to_dev(x, torch.float32) for x in parts), L, causal)
+    torch.cuda.synchronize()
+    og, lg = dmha.unstack_emulated(out.cpu().numpy(), lse.cpu().numpy(), L, layout)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(og, lg, ref_o, ref_l, "fp32", f"fp32 ring P={P} {layout} causal={causal} D={D}")

@@ -5,7 +5,7 @@
   python tools/ncu_kernels.py headpar   # NEXT-1 pack/unpack at C4, P=8 (emulated exchange)
   python tools/ncu_kernels.py combine   # a4 separate LSE combine at a C4 P=8 shard
 
-Used by tools/gpu_r2z.sh as `ncu --set full -k regex:<kernel> -s 2 -c 1 python tools/ncu_kernels.py X`.
+Used by tools/gpu_runs/gpu_r2z.sh as `ncu --set full -k regex:<kernel> -s 2 -c 1 python tools/ncu_kernels.py X`.
 """
 import sys
 from pathlib import Path
