@@ -62,9 +62,16 @@
 #endif
 #endif
 
-// Tiles per TMEM accumulation chunk of O (measurement knob; see kFlush).
-#ifndef DMHA_TF32_FLUSH
-#define DMHA_TF32_FLUSH 4
+// Keys per TMEM accumulation chunk of O (see kFlush; measurement knob).
+#ifndef DMHA_TF32_FLUSH_KEYS
+#define DMHA_TF32_FLUSH_KEYS 512
+#endif
+// K / V^T ring slots (measurement knobs; 2 + 2 measured fastest at both D)
+#ifndef DMHA_TF32_KST
+#define DMHA_TF32_KST 2
+#endif
+#ifndef DMHA_TF32_VST
+#define DMHA_TF32_VST 2
 #endif
 
 namespace dmha {
@@ -76,7 +83,7 @@ constexpr float kTf32RescaleThreshold = 8.0f;  // log2 units, as the bf16 kernel
 template <int D>
 struct Tf32Cfg {
   static constexpr int kBN = D == 64 ? 64 : 32;  // keys per tile
-  static constexpr int kKST = 3, kVST = 2;        // ring slots
+  static constexpr int kKST = DMHA_TF32_KST, kVST = DMHA_TF32_VST;  // ring slots
   static constexpr int kKOp = kBN * D * 4;        // one of K hi / lo
   static constexpr int kVOp = D * kBN * 4;        // one of V^T hi / lo
   static constexpr int kKOff = 0;
@@ -92,9 +99,12 @@ struct Tf32Cfg {
   static constexpr int kCols = kBN / kHalves;  // score columns per half
   static constexpr int kRedOff = kMOff + kBM * D * 4;
   static constexpr int kBarOff = kRedOff + (kHalves == 2 ? 6 * kBM * 4 : 0);
-  // PV restarts its TMEM accumulator every kFlush tiles after the softmax
-  // threads have added the partial into the master copy (see the kernel)
-  static constexpr int kFlush = DMHA_TF32_FLUSH;
+  // PV restarts its TMEM accumulator every kFlush tiles (512 keys) after the
+  // softmax threads have added the partial into the master copy (see the
+  // kernel): error 3.6e-6 (D = 64) / 3.8e-6 (D = 128) rel L2 at any length,
+  // the flush's wait for PV(j-1) paid once per 512 keys
+  static constexpr int kFlush = DMHA_TF32_FLUSH_KEYS / kBN;
+  static_assert(kFlush >= 1, "flush interval");
   // kfull[KST] kempty[KST] vfull[VST] vempty[VST] sfull[2] pready[2] oready
   // ofinal qready
   static constexpr int kNumBars = 2 * kKST + 2 * kVST + 7;

@@ -1,5 +1,5 @@
 """Accuracy and time of the 3xTF32 kernel vs its O flush interval (variant
-builds -DDMHA_TF32_FLUSH=G under paper_2302_06218_b200/ab/f<G>/, loaded via
+builds -DDMHA_TF32_FLUSH_KEYS=K under paper_2302_06218_b200/ab/<name>/, loaded via
 DMHA_LIB): sampled rows of a C2-shaped fp32 forward against the fp64 oracle.
 Usage (one variant per process): DMHA_LIB=... python tools/tf32_flush_sweep.py L H D causal"""
 import sys
