@@ -643,3 +643,22 @@ def test_fp32_ring_emulated_many_tiles(oracle_mod, P, layout, causal, D, extra):
     og, lg = dmha.unstack_emulated(out.cpu().numpy(), lse.cpu().numpy(), L, layout)
     ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
     assert_parity(og, lg, ref_o, ref_l, "fp32", f"fp32 ring P={P} {layout} causal={causal} D={D}")
+
+
+@pytest.mark.parametrize("P,layout,causal,D", [(2, "contiguous", False, 64), (4, "zigzag", True, 128)])
+def test_headpar_emulated_fp32(oracle_mod, P, layout, causal, D):
+    """NEXT-1 on the fp32 path: the pack / all-to-all / unpack kernels move
+    4-byte elements and each rank's local attention (all L keys, H/P heads)
+    runs the 3xTF32 kernel with its split-operand scratch sized for L keys —
+    against the oracle at the fp32 tolerance."""
+    ensure_lib("fp32")
+    L, H = 1024 * P, 2 * P
+    q, k, v = inputs.qkv(L, H, D, seed=650 + P, dtype="fp32")
+    parts = [np.stack([dmha.shard(x, P, r, layout) for r in range(P)]) for x in (q, k, v)]
+    out, lse = dmha.forward_headpar_emulated(P, layout, *(to_dev(p, torch.float32) for p in parts),
+                                             L, causal)
+    torch.cuda.synchronize()
+    og = dmha.unshard(list(out.cpu().numpy()), L, layout)
+    lg = dmha.unshard([x.T for x in lse.cpu().numpy()], L, layout).T
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(og, lg, ref_o, ref_l, "fp32", f"fp32 headpar P={P} {layout} causal={causal} D={D}")
