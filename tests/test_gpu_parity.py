@@ -565,9 +565,26 @@ def test_forward_captures_into_cuda_graph(lib_bf16, case):
         P, L, H, D, causal, layout = 1, 65536, 4, 128, True, "contiguous"
     else:
         P, L, H, D, causal, layout = 4, 4096, 2, 128, True, "zigzag"
-    shape = (L, H, D) if P == 1 else (P, L // P, H, D)
-    lshape = (H, L) if P == 1 else (P, H, L // P)
-    q, k, v = (torch.empty(shape, dtype=torch.bfloat16, device="cuda") for _ in range(3))
+    _graph_capture_case(P, L, H, D, causal, layout, torch.bfloat16, case)
+
+
+@pytest.mark.parametrize("P,L,H,D,causal,layout", [(1, 3000, 3, 64, True, "contiguous"),
+                                                   (3, 3001, 2, 128, False, "contiguous")])
+def test_fp32_forward_captures_into_cuda_graph(P, L, H, D, causal, layout):
+    """The fp32 path in a CUDA graph: dmha_reserve also pre-allocates the
+    3xTF32 split-operand scratch, so the split pre-pass + attention (+ the
+    ring's copies and combines) capture and replay bit-identically."""
+    ensure_lib("fp32")
+    _graph_capture_case(P, L, H, D, causal, layout, torch.float32, f"fp32 P={P}")
+
+
+def _graph_capture_case(P, L, H, D, causal, layout, tdt, case):
+    if P == 1:
+        shape, lshape = (L, H, D), (H, L)
+    else:
+        rows = max(dmha.shard_rows(L, P, r, layout) for r in range(P))
+        shape, lshape = (P, rows, H, D), (P, H, rows)
+    q, k, v = (torch.empty(shape, dtype=tdt, device="cuda") for _ in range(3))
     out = torch.empty_like(q)
     lse = torch.empty(lshape, dtype=torch.float32, device="cuda")
     dmha.reserve(L, D, H, world_size=P)
