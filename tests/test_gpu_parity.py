@@ -679,3 +679,23 @@ def test_headpar_emulated_fp32(oracle_mod, P, layout, causal, D):
     lg = dmha.unshard([x.T for x in lse.cpu().numpy()], L, layout).T
     ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
     assert_parity(og, lg, ref_o, ref_l, "fp32", f"fp32 headpar P={P} {layout} causal={causal} D={D}")
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_fp32_host_path_pipelined(oracle_mod, causal):
+    """dmha_forward_host on the fp32 path at L >= 65536 (copies pipelined with
+    Q row chunks; one K/V block, as the fp32 path has no fused combine): every
+    row is attended over all keys in one launch, so the result equals the
+    device path bit for bit; sampled rows against the oracle."""
+    ensure_lib("fp32")
+    L, H, D = 70000, 2, 64
+    q, k, v = inputs.qkv(L, H, D, seed=72, dtype="fp32")
+    a_o, a_l = run_p1(q, k, v, causal, torch.float32)
+    hq, hk, hv = (torch.from_numpy(x).pin_memory() for x in (q, k, v))
+    ho, hl = dmha.forward_host(hq, hk, hv, L, causal)
+    ho, hl = ho.numpy(), hl.numpy()
+    np.testing.assert_array_equal(ho, a_o)
+    np.testing.assert_array_equal(hl, a_l)
+    rows = _sample_rows(L, [17408, 35072], 64, seed=3)
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal, rows=rows)
+    assert_parity(ho[rows], hl[:, rows], ref_o, ref_l, "fp32", f"fp32 host pipelined causal={causal}")
