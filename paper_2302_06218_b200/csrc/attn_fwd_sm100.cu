@@ -198,13 +198,19 @@ __device__ __forceinline__ int num_kv_tiles(const Params& p, int64_t m0) {
 // mbarrier wait of the attention kernel: D = 128 (power-capped, chain-bound)
 // sleeps on the barrier, D = 64 (wake-up latency on the critical path)
 // polls — measured, see ptx::mbar_try_wait_sleep.
-template <int D>
+template <int D, int kSleepD64 = 0>
 __device__ __forceinline__ void kwait(uint64_t* bar, uint32_t parity) {
-  if constexpr (D == 128)
+  if constexpr (D == 128 || kSleepD64)
     ptx::mbar_wait_sleep(bar, parity);
   else
     ptx::mbar_wait(bar, parity);
 }
+#ifndef DMHA_PROD_SLEEP
+#define DMHA_PROD_SLEEP 0  // measurement knob: D = 64 TMA producer sleeps too
+#endif
+#ifndef DMHA_MMA_SLEEP
+#define DMHA_MMA_SLEEP 0   // measurement knob: D = 64 MMA issuer sleeps too
+#endif
 
 template <int D, int kEmu, bool kSplit, int kIss, bool kPS>
 __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
             const int slot = (which == 0 ? 0 : C::kKSt) + j % nst;
             const uint32_t ph = static_cast<uint32_t>((j / nst) & 1);
             trace_x(p, 5 + 9 * which, j);
-            kwait<D>(&kv_empty[slot], ph ^ 1);
+            kwait<D, DMHA_PROD_SLEEP>(&kv_empty[slot], ph ^ 1);
             trace_x(p, 6 + 9 * which, j);
             ptx::mbar_arrive_expect_tx(&kv_full[slot], C::kTileBytes);
             const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
@@ -328,7 +334,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         for (int j = 0; j < nkv; ++j) {
           for (int which = 0; which < 2; ++which) {
             trace_x(p, 5 + 9 * which, j);
-            kwait<D>(&kv_empty[stage], phase ^ 1);
+            kwait<D, DMHA_PROD_SLEEP>(&kv_empty[stage], phase ^ 1);
             trace_x(p, 6 + 9 * which, j);
             ptx::mbar_arrive_expect_tx(&kv_full[stage], C::kTileBytes);
             const CUtensorMap* tm = which == 0 ? &tm_k : &tm_v;
@@ -409,9 +415,9 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         auto kpar = [](int t) { return static_cast<uint32_t>((t / C::kKSt) & 1); };
         auto vslot = [](int t) { return C::kKSt + t % C::kVSt; };
         auto vpar = [](int t) { return static_cast<uint32_t>((t / C::kVSt) & 1); };
-        kwait<D>(q_full, 0);
+        kwait<D, DMHA_MMA_SLEEP>(q_full, 0);
         if (do_s) {
-          kwait<D>(&kv_full[kslot(0)], kpar(0));
+          kwait<D, DMHA_MMA_SLEEP>(&kv_full[kslot(0)], kpar(0));
           ptx::tc_fence_after();
           for (int g = g_lo; g < g_hi; ++g) {
             qk(g, kslot(0));
@@ -423,10 +429,10 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
           const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
           if (do_s && j < nkv) {  // S_g(j): needs K_j and S_g(j-1) consumed
             trace_x(p, 9 * g_lo + 0, j);
-            kwait<D>(&kv_full[kslot(j)], kpar(j));
+            kwait<D, DMHA_MMA_SLEEP>(&kv_full[kslot(j)], kpar(j));
             trace_x(p, 9 * g_lo + 1, j);
             for (int g = g_lo; g < g_hi; ++g) {
-              kwait<D>(&s_free[g], ppar);
+              kwait<D, DMHA_MMA_SLEEP>(&s_free[g], ppar);
               if (g == g_lo) trace_x(p, 9 * g_lo + 2, j);
               ptx::tc_fence_after();
               qk(g, kslot(j));
@@ -436,10 +442,10 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
             ptx::mma_commit(&kv_empty[kslot(j)]);
           }
           if (do_pv) {  // PV_g(j-1): needs V_{j-1} and P_g(j-1)
-            kwait<D>(&kv_full[vslot(j - 1)], vpar(j - 1));
+            kwait<D, DMHA_MMA_SLEEP>(&kv_full[vslot(j - 1)], vpar(j - 1));
             trace_x(p, 9 * g_lo + 3, j - 1);
             for (int g = g_lo; g < g_hi; ++g) {
-              kwait<D>(&p_ready[g], ppar);
+              kwait<D, DMHA_MMA_SLEEP>(&p_ready[g], ppar);
               trace_stamp(p, 4 + g, j - 1);
               ptx::tc_fence_after();
               pv_sep(g, vslot(j - 1), j > 1);
@@ -458,8 +464,8 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         const int g = warp - kMmaWarp;
         auto slot_of = [](int item) { return item % C::kStages; };
         auto par_of = [](int item) { return static_cast<uint32_t>((item / C::kStages) & 1); };
-        kwait<D>(q_full, 0);
-        kwait<D>(&kv_full[slot_of(0)], par_of(0));
+        kwait<D, DMHA_MMA_SLEEP>(q_full, 0);
+        kwait<D, DMHA_MMA_SLEEP>(&kv_full[slot_of(0)], par_of(0));
         ptx::tc_fence_after();
         qk(g, slot_of(0));
         ptx::mma_commit(&s_full[g]);
@@ -467,9 +473,9 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         for (int j = 1; j <= nkv; ++j) {
           const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
           const int iv = 2 * (j - 1) + 1, ik = 2 * j;
-          kwait<D>(&kv_full[slot_of(iv)], par_of(iv));
-          if (j < nkv) kwait<D>(&kv_full[slot_of(ik)], par_of(ik));
-          kwait<D>(&p_ready[g], ppar);
+          kwait<D, DMHA_MMA_SLEEP>(&kv_full[slot_of(iv)], par_of(iv));
+          if (j < nkv) kwait<D, DMHA_MMA_SLEEP>(&kv_full[slot_of(ik)], par_of(ik));
+          kwait<D, DMHA_MMA_SLEEP>(&p_ready[g], ppar);
           trace_stamp(p, 4 + g, j - 1);
           ptx::tc_fence_after();
           pv(g, slot_of(iv), j > 1);
@@ -488,10 +494,10 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       uint32_t phase = 0;
       auto advance = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
 
-      kwait<D>(q_full, 0);
+      kwait<D, DMHA_MMA_SLEEP>(q_full, 0);
       // j = 0
       int slotK = stage;
-      kwait<D>(&kv_full[slotK], phase);
+      kwait<D, DMHA_MMA_SLEEP>(&kv_full[slotK], phase);
       advance();
       ptx::tc_fence_after();
       qk(0, slotK);
@@ -501,17 +507,17 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
       ptx::mma_commit(&kv_empty[slotK]);
       for (int j = 1; j <= nkv; ++j) {
         const int slotV = stage;  // V_{j-1}
-        kwait<D>(&kv_full[slotV], phase);
+        kwait<D, DMHA_MMA_SLEEP>(&kv_full[slotV], phase);
         advance();
         const bool more = j < nkv;
         int slotK2 = -1;
         if (more) {
           slotK2 = stage;  // K_j
-          kwait<D>(&kv_full[slotK2], phase);
+          kwait<D, DMHA_MMA_SLEEP>(&kv_full[slotK2], phase);
           advance();
         }
         const uint32_t ppar = static_cast<uint32_t>((j - 1) & 1);
-        kwait<D>(&p_ready[0], ppar);
+        kwait<D, DMHA_MMA_SLEEP>(&p_ready[0], ppar);
         trace_stamp(p, 4, j - 1);
         ptx::tc_fence_after();
         pv(0, slotV, j > 1);
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         } else {
           ptx::mma_commit(&o_final[0]);
         }
-        kwait<D>(&p_ready[1], ppar);
+        kwait<D, DMHA_MMA_SLEEP>(&p_ready[1], ppar);
         trace_stamp(p, 5, j - 1);
         ptx::tc_fence_after();
         pv(1, slotV, j > 1);
