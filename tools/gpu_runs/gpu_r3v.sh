@@ -1,0 +1,2 @@
+#!/bin/bash
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
