@@ -233,7 +233,10 @@ int dmha_forward_headpar_emulated(int world_size, int layout, const void *q, con
  * fp32 accumulator O_acc and lse_acc (+ the O_part / lse_part partial buffers
  * when the combine is not fused).  World size 1: 0, except on small grids
  * (< 4 waves of 256-row CTAs, L >= 2048, bf16) where the split-KV launch
- * holds two fp32 partials: 2 * (L*H*D*4 + L*H*4).  Staging buffers of
+ * holds two fp32 partials: 2 * (L*H*D*4 + L*H*4).  dtype fp32 adds, at
+ * every world size, the 3xTF32 kernel's split operands of one key block:
+ * K hi/lo and V^T hi/lo, 2*L_loc*H*D*4 + 2*H*D*ceil4(L_loc)*4 bytes (PAPER.md
+ * :193-211 as 3xTF32, reading R13).  Staging buffers of
  * dmha_forward_host are not included.  A fresh library that runs one forward
  * holds exactly this (dmha_stats.workspace_bytes).  Errors: STATE, INVALID,
  * UNSUPPORTED (D). */
