@@ -21,7 +21,10 @@
  *   lse          : [H, L_loc] fp32 (natural log) — always fp32.
  * Element type of q/k/v/out is fixed by the dtype given to dmha_init:
  *   DMHA_BF16 -> bf16 storage, bf16 tensor-core MMA, fp32 accumulation/softmax;
- *   DMHA_FP32 -> fp32 storage and fp32 FMA-pipe arithmetic (SIMT kernel).
+ *   DMHA_FP32 -> fp32 storage; both contractions as 3xTF32 tcgen05 MMAs (hi/lo
+ *                operand splits), fp32 softmax and accumulation (rel L2 ~4e-6
+ *                against fp64; DMHA_FP32_SIMT=1 selects the SIMT fp32 FMA
+ *                kernel, kept as a cross-check).
  *
  * Ownership: the caller owns q, k, v, out and lse.  q/k/v are read only (the
  * ring sends from them at step 0 and from library buffers afterwards); out and
