@@ -561,7 +561,11 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
     const int64_t row = m0 + g * kBM + r;
     const bool row_ok = row < p.Lq;
     const int64_t qp = pos_of(p.qmap, row_ok ? row : p.Lq - 1);
-    const int64_t klim = key_limit(p, qp);
+    // this row's key limit relative to the launch's first key tile, 32-bit (a
+    // launch's keys fit one GPU: < 2^31): the 64-bit form spilled at the
+    // 96-register cap and was reloaded from local memory every tile
+    const int klim_t =
+        static_cast<int>(key_limit(p, qp) - static_cast<int64_t>(jt0) * kBN);
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tS = tmem + lane_addr + g * kBN;
     const uint32_t tO = tmem + lane_addr + 256 + g * 128 + h * (D / 2);
@@ -582,11 +586,11 @@ __global__ void __launch_bounds__(Roles<kSplit>::kThreads, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&s_free[g]);
       }
-      const int64_t tile_lim = klim - static_cast<int64_t>(jt0 + j) * kBN;
+      const int tile_lim = klim_t - j * kBN;
       const bool masked = !__all_sync(0xffffffffu, tile_lim >= kBN);  // same in both halves
       if (masked) {
-        const int64_t nv64 = tile_lim - h * 64;
-        const int nvalid = nv64 < 0 ? 0 : (nv64 > 64 ? 64 : static_cast<int>(nv64));
+        const int nv = tile_lim - h * 64;
+        const int nvalid = nv < 0 ? 0 : (nv > 64 ? 64 : nv);
 #pragma unroll
         for (int c = 0; c < 64; ++c) s[c] = c < nvalid ? s[c] : -INFINITY;
       }
