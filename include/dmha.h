@@ -367,7 +367,9 @@ int dmha_scatter_rows(const void *y_sel, const int64_t *idx, int64_t n_kept, int
                       void *y_full);
 
 /* Measurement hook: dev_buf (device, >= DMHA_TRACE_WORDS uint64, or NULL to
- * disable) receives clock64 timeline stamps of the bf16 attention kernel
+ * disable) receives, in a library built with -DDMHA_TRACE=1 (tools/trace.py
+ * builds one; the product build compiles the stamps out and leaves the
+ * buffer untouched), clock64 timeline stamps of the bf16 attention kernel
  * (first 4 CTAs of head 0, first 64 KV tiles; events documented in
  * attn_fwd_sm100.cu) and, from word 4096 and only in a library built with
  * -DDMHA_CTA_STAMPS=1, %globaltimer (ns) at the start and end of each of the

@@ -132,13 +132,20 @@ struct Params {
 // [cta < 4][event < 9][tile < 64] clock64 stamps, head 0 only).  Events:
 //  0/2: softmax of Q tile 0/1 saw S(j)   1/3: Q tile 0/1 arrive P(j) ready
 //  4/5: MMA thread saw P0(j)/P1(j) ready   6: MMA thread issued S1(j)
+// Per-tile stamps exist only in a measurement build (-DDMHA_TRACE=1,
+// tools/trace.py builds it): compiled in, the disabled checks and clock reads
+// cost the product kernel 2.6 % at C4 and 2.1 % C5-shaped (one of them sits
+// in the single-thread MMA issue path) — DESIGN.md §5 lesson 32.
+#ifndef DMHA_TRACE
+#define DMHA_TRACE 0
+#endif
 __device__ __forceinline__ void trace_stamp(const Params& p, int ev, int j) {
-  if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < 2 && j < 64)
+  if (DMHA_TRACE && p.trace != nullptr && blockIdx.y == 0 && blockIdx.x < 2 && j < 64)
     p.trace[(blockIdx.x * 9 + ev) * 64 + j] = clock64();
 }
 // Extra events 0..17 of CTA 0 (stored where CTAs 2-3 would be).
 __device__ __forceinline__ void trace_x(const Params& p, int ev, int j) {
-  if (p.trace != nullptr && blockIdx.y == 0 && blockIdx.x == 0 && j < 64)
+  if (DMHA_TRACE && p.trace != nullptr && blockIdx.y == 0 && blockIdx.x == 0 && j < 64)
     p.trace[(18 + ev) * 64 + j] = clock64();
 }
 

@@ -7,7 +7,10 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2302_06218_b200 import dmha  # noqa: E402
+from paper_2302_06218_b200 import build, dmha  # noqa: E402
+
+if "DMHA_LIB" not in os.environ:  # the stamps exist only in a -DDMHA_TRACE=1 build
+    dmha._LIB_PATH = build.build(defines=["DMHA_TRACE=1"], variant="trace")
 
 L = int(os.environ.get("TL", 262144 // 8)); H = 16; D = int(os.environ.get("TD", 128))
 dmha.init(1, 0, None, 0, "bf16", "contiguous")
