@@ -1028,9 +1028,9 @@ cudaError_t launch_de(const LocalAttnArgs& a, cudaStream_t stream) {
 // Measurement knobs (defaults = the measured-fastest configuration):
 //  DMHA_EMU     = pairs (of every 8) of score columns on the FMA-pipe exp2 (0)
 //  DMHA_ISSUERS = MMA-issuing threads: 1 = one for both Q tiles (D = 128
-//                 default), 2 = one per Q tile (D = 64 split-softmax
-//                 default), 3 = split S / PV issuers, 4 = S issuer + one PV
-//                 issuer per Q tile (3 and 4: separate-P schedules only)
+//                 default), 2 = one per Q tile, 3 = split S / PV issuers
+//                 (D = 64 default), 4 = S issuer + one PV issuer per Q tile
+//                 (3 and 4: separate-P schedules only)
 //  DMHA_SPLIT   = 1: split-row softmax (16 softmax warps; D = 64 default)
 //  DMHA_PS      = 1: D = 128 with P in shared memory (separate-P schedule)
 struct PingpongConfig {
@@ -1039,13 +1039,15 @@ struct PingpongConfig {
   bool ps;
 };
 PingpongConfig pingpong_config(int D) {
-  // D = 64 default: the split softmax (16 softmax warps, two per row) with one
-  // MMA issuer per Q tile (DESIGN.md §5 lessons 16-17)
+  // D = 64 default: the split softmax (16 softmax warps, two per row) with
+  // split S / PV issuing warps (DESIGN.md §5 lessons 16-17, 33: one issuer
+  // per Q tile was the round-1 choice; on the final build the S / PV split is
+  // +5 % on small grids and level at million scale)
   PingpongConfig c{D == 64, 1, false};
   if (const char* e = std::getenv("DMHA_SPLIT")) c.split = std::atoi(e) != 0;
   if (const char* e = std::getenv("DMHA_PS")) c.ps = D == 128 && std::atoi(e) != 0;
   if (c.ps) c.split = false;
-  c.iss = D == 64 ? (c.split ? 2 : 3) : 1;
+  c.iss = D == 64 ? 3 : 1;
   if (const char* e = std::getenv("DMHA_ISSUERS")) c.iss = std::atoi(e);
   return c;
 }
