@@ -699,3 +699,23 @@ def test_fp32_host_path_pipelined(oracle_mod, causal):
     rows = _sample_rows(L, [17408, 35072], 64, seed=3)
     ref_o, ref_l = oracle_mod.attention(q, k, v, causal, rows=rows)
     assert_parity(ho[rows], hl[:, rows], ref_o, ref_l, "fp32", f"fp32 host pipelined causal={causal}")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("L,P,causal", [(3, 4, False), (3, 4, True), (5, 8, True), (1, 2, False)])
+def test_emulated_ring_empty_shards(oracle_mod, dtype, L, P, causal):
+    """Fewer rows than ranks (SPEC's equal-as-possible partition leaves some
+    contiguous shards empty): ring steps with zero query rows or zero keys
+    must produce the exact result for the rows that exist."""
+    ensure_lib(dtype)
+    H, D = 2, 64
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    q, k, v = inputs.qkv(L, H, D, seed=2900 + L * 10 + P, dtype=dtype)
+    rows = [dmha.shard_rows(L, P, r, "contiguous") for r in range(P)]
+    assert 0 in rows
+    parts = [dmha.stack_shards(x, P, "contiguous") for x in (q, k, v)]
+    out, lse = dmha.forward_emulated(P, "contiguous", *(to_dev(x, tdt) for x in parts), L, causal)
+    torch.cuda.synchronize()
+    og, lg = dmha.unstack_emulated(out.float().cpu().numpy(), lse.cpu().numpy(), L, "contiguous")
+    ref_o, ref_l = oracle_mod.attention(q, k, v, causal)
+    assert_parity(og, lg, ref_o, ref_l, dtype, f"empty shards {dtype} L={L} P={P} causal={causal}")
