@@ -500,7 +500,7 @@ def test_d128_schedules_on_the_ring(lib_bf16, oracle_mod, monkeypatch, env, P, l
 
 
 FP32_SHAPES = [(1, 1, 64), (37, 2, 64), (128, 1, 128), (200, 3, 128), (512, 4, 64), (777, 2, 64),
-               (1000, 2, 128), (4133, 2, 64), (2085, 2, 128)]
+               (1000, 2, 128), (4133, 2, 64), (2085, 2, 128), (1, 2, 128), (33, 64, 64)]
 
 
 @pytest.mark.parametrize("simt", [False, True])
