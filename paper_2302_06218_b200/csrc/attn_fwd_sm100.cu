@@ -1107,7 +1107,7 @@ bool pingpong_fused_combine_ok(int D) {
   // it runs with per-tile or split issuers (the D = 64 configurations).  The
   // D = 128 split softmax (single issuer) keeps the separate combine pass.
   const PingpongConfig c = pingpong_config(D);
-  return c.ps || !c.split || (D == 64 && (c.iss == 2 || c.iss == 3));
+  return c.ps || !c.split || (D == 64 && (c.iss == 2 || c.iss == 3 || c.iss == 4));
 }
 
 bool attn_fused_combine_supported(int D) {
